@@ -1,0 +1,106 @@
+/* bbdg.h -- C ABI of the B200 BB-DG hot path (libbbdg_cuda.so, sm_100a).
+ *
+ * Drop-in for the per-timestep RHS evaluation and LSRK4 update of the
+ * reference package (Python/numpy, /root/reference/pkg/src/bbdg).  Each entry
+ * point names the reference interface it replaces.  All state pointers are
+ * DEVICE pointers to C-contiguous (4, K, Np) arrays of the context's dtype
+ * (reference FieldState.q layout, solver.py:80-93); `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  No call allocates device
+ * memory on the hot path and no call synchronises the device.  Every function
+ * returns a bbdg_status; bbdg_last_error() holds a message for the calling
+ * thread.  Results are deterministic (owner-computes, no atomics).
+ */
+#ifndef BBDG_H
+#define BBDG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BBDG_OK = 0,
+  BBDG_ERR_ARG = 1,          /* ValueError in the reference (shape, dt <= 0, unknown mode) */
+  BBDG_ERR_UNSUPPORTED = 2,  /* degree outside the compiled range, or missing tables */
+  BBDG_ERR_CUDA = 3          /* CUDA runtime error */
+} bbdg_status;
+
+enum { BBDG_BASIS_BERNSTEIN = 0, BBDG_BASIS_NODAL = 1 };
+enum { BBDG_F32 = 0, BBDG_F64 = 1 };
+/* lift modes of BernsteinRefOps.lift_flux (bernstein.py:457-466); nodal is always dense */
+enum { BBDG_LIFT_FACTORIZED = 0, BBDG_LIFT_OPTIMAL = 1, BBDG_LIFT_DENSE = 2 };
+
+typedef struct bbdg_ctx bbdg_ctx;
+
+/* Library identity. */
+int bbdg_version(void);
+int bbdg_max_degree(void);
+const char* bbdg_last_error(void);
+
+/* Context for one (mesh, degree, basis, dtype): replaces the precomputation in
+ * WaveSystem.__init__ (solver.py:99-123) + ops.astype (bernstein.py:416-434). */
+int bbdg_ctx_create(int N, int basis, int dtype, int64_t K, bbdg_ctx** out);
+void bbdg_ctx_destroy(bbdg_ctx* ctx);
+
+/* Per-element data, float64 host arrays, cast to the context dtype like
+ * WaveSystem.__init__ (solver.py:113-123):
+ *   rst_dx (K,3,3) [k,m,i] = dr_m/dx_i   kappa (K)   inv_rho (K)
+ *   normals (K,4,3)  face_scale (K,4) = jf/jac  tau_p, tau_u (K,4)
+ * and the compact face connectivity replacing the (K,4,Nfp) gather of
+ * build_trace_maps (mesh.py:158-188):
+ *   nbr_elem (K,4) int32   nbr_code (K,4) int8 = f2 | perm<<2 | boundary<<5 | halo<<6 */
+int bbdg_ctx_set_geometry(bbdg_ctx* ctx, const double* rst_dx, const double* kappa, const double* inv_rho,
+                          const double* normals, const double* face_scale, const double* tau_p,
+                          const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code);
+
+/* Lift tables (host, float64): E_L as ELL (Np, width) for the "factorized"
+ * mode (bernstein.py:273-310) and the dense (Np, 4 Nfp) lift for "dense"
+ * (bernstein.py:332-347, nodal.py:411-419).  Either pointer may be NULL. */
+int bbdg_ctx_set_lift_tables(bbdg_ctx* ctx, const int32_t* el_cols, const double* el_vals, int width,
+                             const double* dense_L);
+
+/* Nodal derivative matrices Dr, Ds, Dt (Np, Np) row-major, float64 (nodal.py:397-399). */
+int bbdg_ctx_set_nodal_ops(bbdg_ctx* ctx, const double* Dr, const double* Ds, const double* Dt);
+
+/* Remote face traces for element-partitioned runs: device (4, nhalo, Nfp)
+ * array; faces with the halo bit read slot nbr_elem of it. */
+int bbdg_ctx_set_halo(bbdg_ctx* ctx, const void* halo, int64_t nhalo);
+
+/* WaveSystem.volume_rhs (solver.py:139-158): rhs (=|+=) volume term. */
+int bbdg_volume(bbdg_ctx* ctx, const void* q, void* rhs, int accumulate, void* stream);
+
+/* WaveSystem.surface_rhs (solver.py:166-190): rhs (=|+=) surface term. */
+int bbdg_surface(bbdg_ctx* ctx, const void* q, void* rhs, int lift_mode, int accumulate, void* stream);
+
+/* WaveSystem.rhs (solver.py:192-193): rhs = volume + surface, one pass. */
+int bbdg_rhs(bbdg_ctx* ctx, const void* q, void* rhs, int lift_mode, void* stream);
+
+/* One fused LSRK stage (solver.py:208-213 around WaveSystem.rhs):
+ *   res = rk_a*res + dt*rhs(q_in);  q_out = q_in + rk_b*res.
+ * q_out must not alias q_in (neighbours read q_in during the stage). */
+int bbdg_lsrk_stage(bbdg_ctx* ctx, const void* q_in, void* q_out, void* res, int lift_mode, double rk_a,
+                    double rk_b, double dt, void* stream);
+
+/* The stand-alone LSRK update (solver.py:211-213) over n values, in place:
+ *   res = rk_a*res + dt*rhs;  q += rk_b*res. */
+int bbdg_lsrk_update(int dtype, int64_t n, void* q, void* res, const void* rhs, double rk_a, double rk_b,
+                     double dt, void* stream);
+
+/* lsrk4_step (solver.py:196-214) with the reference's in-place semantics:
+ * zeroes res, runs the five fused stages ping-ponging q <-> q_tmp and leaves
+ * the result in q.  q_tmp and res are caller-owned (4,K,Np) scratch. */
+int bbdg_step(bbdg_ctx* ctx, void* q, void* q_tmp, void* res, double dt, int lift_mode, void* stream);
+
+/* Pack the face traces of (elem, face) pairs (device int32 (n,2)) into
+ * sendbuf (4, n, Nfp) in each face's own canonical order (halo send side). */
+int bbdg_halo_pack(bbdg_ctx* ctx, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream);
+
+/* Introspection used by tests and the benchmark. */
+int bbdg_tile_elems(int N, int dtype);
+int64_t bbdg_kernel_smem(int N, int dtype, int op, int lift, int basis);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BBDG_H */

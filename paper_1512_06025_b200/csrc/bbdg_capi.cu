@@ -1,0 +1,485 @@
+// C ABI of libbbdg_cuda.so: context lifetime, table uploads, dispatch of the
+// tile kernels, the stand-alone LSRK update and the halo packer.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bbdg_common.cuh"
+#include "bbdg_internal.h"
+#include "bbdg_tile.cuh"
+
+struct bbdg_ctx {
+  int N, basis, dtype;
+  int64_t K;
+  int Np, Nfp;
+  int num_sms;
+  void* geo_vol = nullptr;   // T (K,12)
+  void* geo_surf = nullptr;  // T (K,24)
+  int32_t* nbr = nullptr;    // (K,4)
+  int32_t* code = nullptr;   // (K)
+  void* el_vals = nullptr;   // T (Np,w)
+  uint16_t* el_cols = nullptr;
+  int el_w = 0;
+  void* liftT = nullptr;     // T (4Nfp,Np)
+  void* dT = nullptr;        // T (3,Np,Np)
+  const void* halo = nullptr;
+  int64_t nhalo = 0;
+};
+
+namespace bbdg {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+int set_cuda_error(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return BBDG_ERR_CUDA;
+}
+
+static KernelEntry lookup(int dtype, int N, int op, int lift, int basis) {
+#define BBDG_SW(tn)                                  \
+  switch (N) {                                       \
+    case 1: return entry_##tn##_1(op, lift, basis);  \
+    case 2: return entry_##tn##_2(op, lift, basis);  \
+    case 3: return entry_##tn##_3(op, lift, basis);  \
+    case 4: return entry_##tn##_4(op, lift, basis);  \
+    case 5: return entry_##tn##_5(op, lift, basis);  \
+    case 6: return entry_##tn##_6(op, lift, basis);  \
+    case 7: return entry_##tn##_7(op, lift, basis);  \
+    case 8: return entry_##tn##_8(op, lift, basis);  \
+    case 9: return entry_##tn##_9(op, lift, basis);  \
+  }
+  if (dtype == BBDG_F32) { BBDG_SW(f32) }
+  else { BBDG_SW(f64) }
+#undef BBDG_SW
+  return KernelEntry{nullptr, nullptr, 0};
+}
+
+template <typename T> static void* upload(const std::vector<T>& h, int* rc) {
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, std::max<size_t>(h.size(), 1) * sizeof(T));
+  if (e == cudaSuccess && !h.empty()) e = cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    *rc = set_cuda_error(e, "table upload");
+    if (d) cudaFree(d);
+    return nullptr;
+  }
+  return d;
+}
+
+template <typename T> static std::vector<T> cast(const double* src, size_t n) {
+  std::vector<T> v(n);
+  for (size_t i = 0; i < n; ++i) v[i] = static_cast<T>(src[i]);
+  return v;
+}
+
+template <typename T>
+static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa, const double* inv_rho,
+                          const double* normals, const double* face_scale, const double* tau_p,
+                          const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code) {
+  const int64_t K = c->K;
+  std::vector<T> gv((size_t)K * kGeoVol, T(0)), gs((size_t)K * kGeoSurf);
+  std::vector<int32_t> nb((size_t)K * 4), cd((size_t)K);
+  for (int64_t k = 0; k < K; ++k) {
+    for (int j = 0; j < 9; ++j) gv[k * kGeoVol + j] = static_cast<T>(rst_dx[k * 9 + j]);
+    gv[k * kGeoVol + 9] = static_cast<T>(kappa[k]);
+    gv[k * kGeoVol + 10] = static_cast<T>(inv_rho[k]);
+    uint32_t packed = 0;
+    for (int f = 0; f < 4; ++f) {
+      T* g = &gs[k * kGeoSurf + f * 6];
+      for (int i = 0; i < 3; ++i) g[i] = static_cast<T>(normals[(k * 4 + f) * 3 + i]);
+      g[3] = static_cast<T>(face_scale[k * 4 + f]);
+      g[4] = static_cast<T>(tau_p[k * 4 + f]);
+      g[5] = static_cast<T>(tau_u[k * 4 + f]);
+      const int32_t n = nbr_elem[k * 4 + f];
+      const int code = static_cast<uint8_t>(nbr_code[k * 4 + f]);
+      const bool halo = (code >> 6) & 1, bnd = (code >> 5) & 1;
+      if (!bnd && !halo && (n < 0 || n >= K)) return set_error(BBDG_ERR_ARG, "neighbour element out of range");
+      nb[k * 4 + f] = n;
+      packed |= static_cast<uint32_t>(code) << (8 * f);
+    }
+    cd[k] = static_cast<int32_t>(packed);
+  }
+  int rc = BBDG_OK;
+  cudaFree(c->geo_vol);
+  cudaFree(c->geo_surf);
+  cudaFree(c->nbr);
+  cudaFree(c->code);
+  c->geo_vol = upload(gv, &rc);
+  c->geo_surf = upload(gs, &rc);
+  c->nbr = static_cast<int32_t*>(upload(nb, &rc));
+  c->code = static_cast<int32_t*>(upload(cd, &rc));
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// stand-alone LSRK update (K8) and halo pack
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void lsrk_update_kernel(int64_t n, T* __restrict__ q, T* __restrict__ res, const T* __restrict__ rhs,
+                                   T a, T b, T dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T r = res[i] * a;
+    r = r + dt * rhs[i];
+    res[i] = r;
+    q[i] = q[i] + b * r;
+  }
+}
+
+// vectorised body: 16-byte lanes when all three arrays are aligned
+template <typename T, typename V, int W>
+__global__ void lsrk_update_vec_kernel(int64_t nv, V* __restrict__ q, V* __restrict__ res,
+                                       const V* __restrict__ rhs, T a, T b, T dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    V r = res[i], k = __ldg(rhs + i), x = q[i];
+    T* rr = reinterpret_cast<T*>(&r);
+    const T* kk = reinterpret_cast<const T*>(&k);
+    T* xx = reinterpret_cast<T*>(&x);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      rr[j] = rr[j] * a;
+      rr[j] = rr[j] + dt * kk[j];
+      xx[j] = xx[j] + b * rr[j];
+    }
+    res[i] = r;
+    q[i] = x;
+  }
+}
+
+template <typename T>
+static int lsrk_update_t(int64_t n, void* q, void* res, const void* rhs, double a, double b, double dt,
+                         cudaStream_t s, int num_sms) {
+  if (n == 0) return BBDG_OK;
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int W = 16 / sizeof(T);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(res) |
+                         reinterpret_cast<uintptr_t>(rhs)) & 15) == 0;
+  const int threads = 256;
+  if (aligned) {
+    const int64_t nv = n / W;
+    if (nv) {
+      const int64_t grid = std::min<int64_t>((nv + threads - 1) / threads, (int64_t)num_sms * 8);
+      lsrk_update_vec_kernel<T, V, W><<<(unsigned)grid, threads, 0, s>>>(
+          nv, static_cast<V*>(q), static_cast<V*>(res), static_cast<const V*>(rhs), T(a), T(b), T(dt));
+    }
+    const int64_t tail = n - nv * W;
+    if (tail)
+      lsrk_update_kernel<T><<<1, threads, 0, s>>>(tail, static_cast<T*>(q) + nv * W, static_cast<T*>(res) + nv * W,
+                                                  static_cast<const T*>(rhs) + nv * W, T(a), T(b), T(dt));
+  } else {
+    const int64_t grid = std::min<int64_t>((n + threads - 1) / threads, (int64_t)num_sms * 8);
+    lsrk_update_kernel<T><<<(unsigned)grid, threads, 0, s>>>(n, static_cast<T*>(q), static_cast<T*>(res),
+                                                              static_cast<const T*>(rhs), T(a), T(b), T(dt));
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "lsrk update launch");
+}
+
+template <typename T>
+__global__ void halo_pack_kernel(int N, int64_t K, int Np, int Nfp, const T* __restrict__ q, T* __restrict__ out,
+                                 const int32_t* __restrict__ faces, int64_t n) {
+  const int64_t total = n * Nfp;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / Nfp;
+    const int m = (int)(t % Nfp);
+    const int64_t k = faces[2 * i];
+    const int f = faces[2 * i + 1];
+    int b0 = 0, r = m;
+    while (r >= N - b0 + 1) { r -= N - b0 + 1; ++b0; }
+    const int b[3] = {b0, r, N - b0 - r};
+    int a[4], s = 0;
+    for (int v = 0; v < 4; ++v) a[v] = (v == f) ? 0 : b[s++];
+    const int pos = pos3(N, a[0], a[1], a[2]);
+    for (int F = 0; F < 4; ++F) out[(F * n + i) * Nfp + m] = q[(F * K + k) * Np + pos];
+  }
+}
+
+static int num_sms_of_current_device() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return n;
+}
+
+template <typename T> static Params<T> make_params(const bbdg_ctx* c) {
+  Params<T> p{};
+  p.K = c->K;
+  p.geo_vol = static_cast<const T*>(c->geo_vol);
+  p.geo_surf = static_cast<const T*>(c->geo_surf);
+  p.nbr = c->nbr;
+  p.code = c->code;
+  p.halo = static_cast<const T*>(c->halo);
+  p.nhalo = c->nhalo;
+  p.el_vals = static_cast<const T*>(c->el_vals);
+  p.el_cols = c->el_cols;
+  p.el_w = c->el_w;
+  p.liftT = static_cast<const T*>(c->liftT);
+  p.dT = static_cast<const T*>(c->dT);
+  return p;
+}
+
+}  // namespace bbdg
+
+using namespace bbdg;
+
+static int check_ctx(const bbdg_ctx* c) {
+  if (!c) return set_error(BBDG_ERR_ARG, "null context");
+  if (!c->geo_vol) return set_error(BBDG_ERR_UNSUPPORTED, "geometry not uploaded (bbdg_ctx_set_geometry)");
+  return BBDG_OK;
+}
+
+static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
+  if (c->basis == BBDG_BASIS_NODAL) {
+    // WaveSystem forces "dense" for the nodal basis (solver.py:168-169)
+    lift = BBDG_LIFT_DENSE;
+    if (surf && !c->liftT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal dense lift not uploaded");
+    if (!c->dT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal derivative matrices not uploaded");
+    return BBDG_OK;
+  }
+  if (lift < 0 || lift > 2) return set_error(BBDG_ERR_ARG, "unknown lift mode");
+  if (surf && lift == BBDG_LIFT_FACTORIZED && !c->el_vals)
+    return set_error(BBDG_ERR_UNSUPPORTED, "E_L table not uploaded (bbdg_ctx_set_lift_tables)");
+  if (surf && lift == BBDG_LIFT_DENSE && !c->liftT)
+    return set_error(BBDG_ERR_UNSUPPORTED, "dense lift not uploaded (bbdg_ctx_set_lift_tables)");
+  return BBDG_OK;
+}
+
+template <typename T>
+static int run(bbdg_ctx* c, int op, int lift, Params<T>& p, void* stream) {
+  KernelEntry k = lookup(c->dtype, c->N, op, lift, c->basis);
+  if (!k.launch) return set_error(BBDG_ERR_UNSUPPORTED, "no kernel for this (op, lift, basis)");
+  return k.launch(&p, static_cast<cudaStream_t>(stream), c->num_sms);
+}
+
+extern "C" {
+
+int bbdg_version(void) { return 1; }
+int bbdg_max_degree(void) { return kMaxDegree; }
+const char* bbdg_last_error(void) { return g_err.c_str(); }
+
+int bbdg_ctx_create(int N, int basis, int dtype, int64_t K, bbdg_ctx** out) {
+  if (!out) return set_error(BBDG_ERR_ARG, "null output pointer");
+  *out = nullptr;
+  if (N < 1 || N > kMaxDegree) return set_error(BBDG_ERR_UNSUPPORTED, "degree outside the compiled range 1..9");
+  if (basis != BBDG_BASIS_BERNSTEIN && basis != BBDG_BASIS_NODAL) return set_error(BBDG_ERR_ARG, "unknown basis");
+  if (dtype != BBDG_F32 && dtype != BBDG_F64) return set_error(BBDG_ERR_ARG, "unknown dtype");
+  if (K < 0 || K >= (int64_t(1) << 31)) return set_error(BBDG_ERR_ARG, "K must lie in [0, 2^31)");
+  bbdg_ctx* c = new bbdg_ctx();
+  c->N = N;
+  c->basis = basis;
+  c->dtype = dtype;
+  c->K = K;
+  c->Np = tet_dim(N);
+  c->Nfp = tri_dim(N);
+  c->num_sms = num_sms_of_current_device();
+  *out = c;
+  return BBDG_OK;
+}
+
+void bbdg_ctx_destroy(bbdg_ctx* c) {
+  if (!c) return;
+  cudaFree(c->geo_vol);
+  cudaFree(c->geo_surf);
+  cudaFree(c->nbr);
+  cudaFree(c->code);
+  cudaFree(c->el_vals);
+  cudaFree(c->el_cols);
+  cudaFree(c->liftT);
+  cudaFree(c->dT);
+  delete c;
+}
+
+int bbdg_ctx_set_geometry(bbdg_ctx* c, const double* rst_dx, const double* kappa, const double* inv_rho,
+                          const double* normals, const double* face_scale, const double* tau_p,
+                          const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code) {
+  if (!c || !rst_dx || !kappa || !inv_rho || !normals || !face_scale || !tau_p || !tau_u || !nbr_elem || !nbr_code)
+    return set_error(BBDG_ERR_ARG, "null argument");
+  return c->dtype == BBDG_F32
+             ? set_geometry_t<float>(c, rst_dx, kappa, inv_rho, normals, face_scale, tau_p, tau_u, nbr_elem, nbr_code)
+             : set_geometry_t<double>(c, rst_dx, kappa, inv_rho, normals, face_scale, tau_p, tau_u, nbr_elem,
+                                      nbr_code);
+}
+
+int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* el_vals, int width,
+                             const double* dense_L) {
+  if (!c) return set_error(BBDG_ERR_ARG, "null context");
+  const int Np = c->Np, Nfp = c->Nfp;
+  int rc = BBDG_OK;
+  if (el_cols && el_vals) {
+    if (width < 1 || width > 4 * Nfp) return set_error(BBDG_ERR_ARG, "bad E_L width");
+    std::vector<uint16_t> cols((size_t)Np * width);
+    for (size_t i = 0; i < cols.size(); ++i) {
+      if (el_cols[i] < 0 || el_cols[i] >= 4 * Nfp) return set_error(BBDG_ERR_ARG, "E_L column out of range");
+      cols[i] = static_cast<uint16_t>(el_cols[i]);
+    }
+    cudaFree(c->el_vals);
+    cudaFree(c->el_cols);
+    c->el_vals = c->dtype == BBDG_F32 ? upload(cast<float>(el_vals, cols.size()), &rc)
+                                      : upload(cast<double>(el_vals, cols.size()), &rc);
+    c->el_cols = static_cast<uint16_t*>(upload(cols, &rc));
+    c->el_w = width;
+  }
+  if (dense_L) {
+    std::vector<double> t((size_t)4 * Nfp * Np);
+    for (int a = 0; a < Np; ++a)
+      for (int j = 0; j < 4 * Nfp; ++j) t[(size_t)j * Np + a] = dense_L[(size_t)a * 4 * Nfp + j];
+    cudaFree(c->liftT);
+    c->liftT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
+                                    : upload(cast<double>(t.data(), t.size()), &rc);
+  }
+  return rc;
+}
+
+int bbdg_ctx_set_nodal_ops(bbdg_ctx* c, const double* Dr, const double* Ds, const double* Dt) {
+  if (!c || !Dr || !Ds || !Dt) return set_error(BBDG_ERR_ARG, "null argument");
+  const int Np = c->Np;
+  std::vector<double> t((size_t)3 * Np * Np);
+  const double* D[3] = {Dr, Ds, Dt};
+  for (int d = 0; d < 3; ++d)
+    for (int a = 0; a < Np; ++a)
+      for (int b = 0; b < Np; ++b) t[((size_t)d * Np + b) * Np + a] = D[d][(size_t)a * Np + b];
+  int rc = BBDG_OK;
+  cudaFree(c->dT);
+  c->dT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
+                               : upload(cast<double>(t.data(), t.size()), &rc);
+  return rc;
+}
+
+int bbdg_ctx_set_halo(bbdg_ctx* c, const void* halo, int64_t nhalo) {
+  if (!c || nhalo < 0 || (nhalo > 0 && !halo)) return set_error(BBDG_ERR_ARG, "bad halo");
+  c->halo = halo;
+  c->nhalo = nhalo;
+  return BBDG_OK;
+}
+
+#define BBDG_DISPATCH(EXPR)                                                 \
+  (c->dtype == BBDG_F32 ? [&]() { using T = float; EXPR; }() : [&]() { using T = double; EXPR; }())
+
+int bbdg_volume(bbdg_ctx* c, const void* q, void* rhs, int accumulate, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
+  int lift = BBDG_LIFT_OPTIMAL;
+  if (c->basis == BBDG_BASIS_NODAL) {
+    if (int rc = check_lift(c, lift, false)) return rc;
+  }
+  return BBDG_DISPATCH({
+    Params<T> p = make_params<T>(c);
+    p.q = static_cast<const T*>(q);
+    p.out = static_cast<T*>(rhs);
+    p.accumulate = accumulate;
+    return run<T>(c, OP_VOLUME, lift, p, stream);
+  });
+}
+
+int bbdg_surface(bbdg_ctx* c, const void* q, void* rhs, int lift, int accumulate, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (int rc = check_lift(c, lift, true)) return rc;
+  return BBDG_DISPATCH({
+    Params<T> p = make_params<T>(c);
+    p.q = static_cast<const T*>(q);
+    p.out = static_cast<T*>(rhs);
+    p.accumulate = accumulate;
+    return run<T>(c, OP_SURFACE, lift, p, stream);
+  });
+}
+
+int bbdg_rhs(bbdg_ctx* c, const void* q, void* rhs, int lift, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q");
+  if (int rc = check_lift(c, lift, true)) return rc;
+  return BBDG_DISPATCH({
+    Params<T> p = make_params<T>(c);
+    p.q = static_cast<const T*>(q);
+    p.out = static_cast<T*>(rhs);
+    return run<T>(c, OP_RHS, lift, p, stream);
+  });
+}
+
+int bbdg_lsrk_stage(bbdg_ctx* c, const void* q_in, void* q_out, void* res, int lift, double rk_a, double rk_b,
+                    double dt, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!q_in || !q_out || !res) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (q_in == q_out) return set_error(BBDG_ERR_ARG, "q_out must not alias q_in");
+  if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  if (int rc = check_lift(c, lift, true)) return rc;
+  return BBDG_DISPATCH({
+    Params<T> p = make_params<T>(c);
+    p.q = static_cast<const T*>(q_in);
+    p.out = static_cast<T*>(q_out);
+    p.res = static_cast<T*>(res);
+    p.rk_a = T(rk_a);
+    p.rk_b = T(rk_b);
+    p.dt = T(dt);
+    return run<T>(c, OP_STAGE, lift, p, stream);
+  });
+}
+
+int bbdg_lsrk_update(int dtype, int64_t n, void* q, void* res, const void* rhs, double rk_a, double rk_b, double dt,
+                     void* stream) {
+  if (n < 0 || (n > 0 && (!q || !res || !rhs))) return set_error(BBDG_ERR_ARG, "bad update arguments");
+  if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  const int sms = num_sms_of_current_device();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == BBDG_F32) return lsrk_update_t<float>(n, q, res, rhs, rk_a, rk_b, dt, s, sms);
+  if (dtype == BBDG_F64) return lsrk_update_t<double>(n, q, res, rhs, rk_a, rk_b, dt, s, sms);
+  return set_error(BBDG_ERR_ARG, "unknown dtype");
+}
+
+// Carpenter-Kennedy five-stage LSRK4 coefficients (solver.py:25-51)
+static const double kRK4A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                                -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+static const double kRK4B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                                1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                                2277821191437.0 / 14882151754819.0};
+
+int bbdg_step(bbdg_ctx* c, void* q, void* q_tmp, void* res, double dt, int lift, void* stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!q || !q_tmp || !res) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = (size_t)4 * c->K * c->Np * (c->dtype == BBDG_F32 ? 4 : 8);
+  cudaError_t e = cudaMemsetAsync(res, 0, bytes, s);
+  if (e != cudaSuccess) return set_cuda_error(e, "res zeroing");
+  void* buf[2] = {q, q_tmp};
+  for (int st = 0; st < 5; ++st) {
+    int rc = bbdg_lsrk_stage(c, buf[st & 1], buf[(st + 1) & 1], res, lift, kRK4A[st], kRK4B[st], dt, stream);
+    if (rc) return rc;
+  }
+  e = cudaMemcpyAsync(q, q_tmp, bytes, cudaMemcpyDeviceToDevice, s);
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "final stage copy");
+}
+
+int bbdg_halo_pack(bbdg_ctx* c, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream) {
+  if (!c || (n > 0 && (!q || !sendbuf || !faces))) return set_error(BBDG_ERR_ARG, "bad halo pack arguments");
+  if (n == 0) return BBDG_OK;
+  const int threads = 256;
+  const int64_t grid = std::min<int64_t>((n * c->Nfp + threads - 1) / threads, (int64_t)c->num_sms * 8);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->dtype == BBDG_F32)
+    halo_pack_kernel<float><<<(unsigned)grid, threads, 0, s>>>(c->N, c->K, c->Np, c->Nfp, static_cast<const float*>(q),
+                                                               static_cast<float*>(sendbuf), faces, n);
+  else
+    halo_pack_kernel<double><<<(unsigned)grid, threads, 0, s>>>(c->N, c->K, c->Np, c->Nfp,
+                                                                static_cast<const double*>(q),
+                                                                static_cast<double*>(sendbuf), faces, n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "halo pack launch");
+}
+
+int bbdg_tile_elems(int N, int dtype) {
+  KernelEntry k = lookup(dtype, N, OP_STAGE, LIFT_OPTIMAL, BASIS_BERNSTEIN);
+  return k.launch ? k.tile_elems : -1;
+}
+
+int64_t bbdg_kernel_smem(int N, int dtype, int op, int lift, int basis) {
+  KernelEntry k = lookup(dtype, N, op, lift, basis);
+  return k.smem ? k.smem() : -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,485 @@
+"""Drop-in solver API (reference ``/root/reference/pkg/src/bbdg/solver.py``).
+
+``WaveSystem``, ``lsrk4_step`` and ``integrate`` keep the reference's
+signatures and semantics, but every RHS evaluation and LSRK update runs in
+``libbbdg_cuda.so`` (hand-written sm_100a kernels behind the C ABI of
+``include/bbdg.h``).  States may be numpy arrays (copied host<->device around
+each call, as a drop-in for the reference's numpy-in/numpy-out contract) or
+CUDA torch tensors (device-resident; no copies).  There is no CPU fallback:
+constructing a ``WaveSystem`` without the library or a CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .mesh import Mesh, build_trace_maps
+from .modal import tet_rule
+from .nodal import NodalRefOps, nodal_to_bernstein
+
+# Carpenter-Kennedy five-stage LSRK4 (reference solver.py:24-51)
+RK4A = np.array([0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                 -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0])
+RK4B = np.array([1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                 1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                 2277821191437.0 / 14882151754819.0])
+RK4C = np.array([0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+                 2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0])
+
+_SQRT3 = np.sqrt(3.0)
+LIFT_MODES = ("factorized", "optimal", "dense")
+
+
+def _torch():
+    import torch  # plumbing only: device buffers, streams, copies
+
+    if not torch.cuda.is_available():
+        raise _lib.BBDGError("no CUDA device: the BB-DG hot path runs only on the GPU (no CPU fallback)")
+    return torch
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass(frozen=True)
+class Materials:
+    """Piecewise-constant bulk modulus and density (reference solver.py:56-77)."""
+
+    kappa: np.ndarray
+    rho: np.ndarray
+
+    @classmethod
+    def homogeneous(cls, K: int, kappa: float = 1.0, rho: float = 1.0):
+        return cls(np.full(K, float(kappa)), np.full(K, float(rho)))
+
+    def __post_init__(self):
+        if np.any(np.asarray(self.kappa) <= 0) or np.any(np.asarray(self.rho) <= 0):
+            raise ValueError("kappa and rho must be positive")
+
+    @property
+    def c(self):
+        return np.sqrt(self.kappa / self.rho)
+
+    @property
+    def rho_c(self):
+        return self.rho * self.c
+
+
+@dataclass
+class FieldState:
+    """Coefficients of (p, u1, u2, u3), q shape (4, K, Np): numpy or CUDA tensor."""
+
+    q: object
+    basis: str
+    time: float = 0.0
+
+    @property
+    def precision(self) -> str:
+        dt = self.q.dtype
+        return "single" if str(dt) in ("float32", "torch.float32") else "double"
+
+    def copy(self) -> "FieldState":
+        return FieldState(self.q.clone() if _is_tensor(self.q) else self.q.copy(), self.basis, self.time)
+
+
+class WaveSystem:
+    """Mesh + operators + materials bound to a device context (solver.py:96-193)."""
+
+    def __init__(self, mesh: Mesh, ops, materials: Materials, dtype=np.float64):
+        if len(materials.kappa) != mesh.K:
+            raise ValueError("materials sized for a different mesh")
+        self.mesh = mesh
+        self.ops_double = ops
+        self.dtype = np.dtype(dtype).type
+        if self.dtype not in (np.float32, np.float64):
+            raise ValueError("dtype must be float32 or float64")
+        self.ops = ops.astype(self.dtype)
+        self.mat = materials
+        K = mesh.K
+        # per-face constants exactly as the reference forms them (solver.py:113-123)
+        rc = materials.rho_c
+        mean_rc = 0.5 * (rc[:, None] + rc[mesh.etoe])
+        self._tau_p64 = np.ascontiguousarray(1.0 / mean_rc)
+        self._tau_u64 = np.ascontiguousarray(mean_rc)
+        self._fscale64 = np.ascontiguousarray(mesh.jf / mesh.jac[:, None])
+        self.tau_p = self._tau_p64.astype(self.dtype)[:, :, None]
+        self.tau_u = self._tau_u64.astype(self.dtype)[:, :, None]
+        self.face_scale = self._fscale64.astype(self.dtype)[:, :, None]
+        self.normals = mesh.normals.astype(self.dtype)
+        self.rst_dx = mesh.rst_dx.astype(self.dtype)
+        self.kappa = materials.kappa.astype(self.dtype)[:, None]
+        self.inv_kappa = (1.0 / materials.kappa).astype(self.dtype)[:, None]
+        self.inv_rho = (1.0 / materials.rho).astype(self.dtype)[:, None]
+        self._gather = None
+        self._torch = _torch()
+        self._lib = _lib.load()
+        self._ctx = None
+        self._ctx = self._create_context(mesh, materials)
+
+    # ---------------------------------------------------------------- context
+    def _create_context(self, mesh: Mesh, materials: Materials):
+        L = self._lib
+        ctx = C.c_void_p()
+        _lib.check(L.bbdg_ctx_create(self.ops.N, _lib.BASIS[self.basis], _lib.DTYPE[np.dtype(self.dtype).name],
+                                     mesh.K, C.byref(ctx)), "bbdg_ctx_create")
+        nbr, code = mesh.face_codes()
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (mesh.rst_dx, materials.kappa, 1.0 / materials.rho, mesh.normals,
+                 self._fscale64, self._tau_p64, self._tau_u64)]
+        nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        code = np.ascontiguousarray(code, dtype=np.int8)
+        _lib.check(L.bbdg_ctx_set_geometry(ctx, *[a.ctypes.data for a in arrs], nbr.ctypes.data, code.ctypes.data),
+                   "bbdg_ctx_set_geometry")
+        if self.basis == "bernstein":
+            cols, vals = self.ops_double.el_ell()
+            dl = np.ascontiguousarray(self.ops_double.dense_L)
+            _lib.check(L.bbdg_ctx_set_lift_tables(ctx, cols.ctypes.data, vals.ctypes.data, cols.shape[1],
+                                                  dl.ctypes.data), "bbdg_ctx_set_lift_tables")
+        else:
+            o = self.ops_double
+            D = [np.ascontiguousarray(x, dtype=np.float64) for x in (o.Dr, o.Ds, o.Dt)]
+            dl = np.ascontiguousarray(o.dense_L, dtype=np.float64)
+            _lib.check(L.bbdg_ctx_set_nodal_ops(ctx, *[d.ctypes.data for d in D]), "bbdg_ctx_set_nodal_ops")
+            _lib.check(L.bbdg_ctx_set_lift_tables(ctx, None, None, 0, dl.ctypes.data), "bbdg_ctx_set_lift_tables")
+        return ctx
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None and _lib._lib is not None:
+            _lib._lib.bbdg_ctx_destroy(ctx)
+            self._ctx = None
+
+    @property
+    def basis(self) -> str:
+        return self.ops.basis
+
+    @property
+    def K(self) -> int:
+        return self.mesh.K
+
+    @property
+    def Np(self) -> int:
+        return self.ops.Np
+
+    @property
+    def gather(self):
+        """Reference-layout flat neighbour gather (K,4,Nfp), built on demand."""
+        if self._gather is None:
+            self._gather = build_trace_maps(self.mesh, self.ops.trace, self.ops.Np)
+        return self._gather[0]
+
+    @property
+    def boundary(self):
+        return self.mesh.boundary
+
+    @property
+    def torch_dtype(self):
+        t = self._torch
+        return t.float32 if self.dtype == np.float32 else t.float64
+
+    def _stream(self):
+        return self._torch.cuda.current_stream().cuda_stream
+
+    # ---------------------------------------------------------------- marshalling
+    def _check(self, state: FieldState):
+        if state.basis != self.basis:
+            raise ValueError(f"state basis {state.basis!r} does not match {self.basis!r}")
+        if tuple(state.q.shape) != (4, self.K, self.ops.Np):
+            raise ValueError("state shaped for a different system")
+
+    def to_device(self, q):
+        """Device tensor view/copy of q in the system dtype (H2D for numpy)."""
+        t = self._torch
+        if _is_tensor(q):
+            if not q.is_cuda:
+                q = q.cuda()
+            if q.dtype != self.torch_dtype:
+                q = q.to(self.torch_dtype)
+            return q.contiguous()
+        a = np.ascontiguousarray(q, dtype=self.dtype)
+        return t.from_numpy(a).to("cuda")
+
+    def empty_state(self):
+        return self._torch.empty((4, self.K, self.ops.Np), dtype=self.torch_dtype, device="cuda")
+
+    def _out(self, dq, like):
+        return dq if _is_tensor(like) else dq.cpu().numpy()
+
+    @staticmethod
+    def _lift_id(lift_mode):
+        if lift_mode not in _lib.LIFT:
+            raise ValueError(f"unknown lift mode {lift_mode!r}")
+        return _lib.LIFT[lift_mode]
+
+    # ---------------------------------------------------------------- device entry points
+    def volume_into(self, q, out, accumulate=False):
+        _lib.check(self._lib.bbdg_volume(self._ctx, q.data_ptr(), out.data_ptr(), int(accumulate), self._stream()),
+                   "bbdg_volume")
+
+    def surface_into(self, q, out, lift_mode="factorized", accumulate=False):
+        _lib.check(self._lib.bbdg_surface(self._ctx, q.data_ptr(), out.data_ptr(), self._lift_id(lift_mode),
+                                          int(accumulate), self._stream()), "bbdg_surface")
+
+    def rhs_into(self, q, out, lift_mode="factorized"):
+        _lib.check(self._lib.bbdg_rhs(self._ctx, q.data_ptr(), out.data_ptr(), self._lift_id(lift_mode),
+                                      self._stream()), "bbdg_rhs")
+
+    def stage_into(self, q_in, q_out, res, a, b, dt, lift_mode="factorized"):
+        _lib.check(self._lib.bbdg_lsrk_stage(self._ctx, q_in.data_ptr(), q_out.data_ptr(), res.data_ptr(),
+                                             self._lift_id(lift_mode), float(a), float(b), float(dt),
+                                             self._stream()), "bbdg_lsrk_stage")
+
+    def step_into(self, q, q_tmp, res, dt, lift_mode="factorized"):
+        _lib.check(self._lib.bbdg_step(self._ctx, q.data_ptr(), q_tmp.data_ptr(), res.data_ptr(), float(dt),
+                                       self._lift_id(lift_mode), self._stream()), "bbdg_step")
+
+    # ---------------------------------------------------------------- reference API
+    def volume_rhs(self, state: FieldState):
+        self._check(state)
+        q = self.to_device(state.q)
+        dq = self._torch.empty_like(q)
+        self.volume_into(q, dq)
+        return self._out(dq, state.q)
+
+    def surface_rhs(self, state: FieldState, lift_mode: str = "factorized"):
+        self._check(state)
+        if self.basis == "nodal":
+            lift_mode = "dense"
+        self._lift_id(lift_mode)
+        q = self.to_device(state.q)
+        dq = self._torch.empty_like(q)
+        self.surface_into(q, dq, lift_mode)
+        return self._out(dq, state.q)
+
+    def rhs(self, state: FieldState, lift_mode: str = "factorized"):
+        self._check(state)
+        if self.basis == "nodal":
+            lift_mode = "dense"
+        self._lift_id(lift_mode)
+        q = self.to_device(state.q)
+        dq = self._torch.empty_like(q)
+        self.rhs_into(q, dq, lift_mode)
+        return self._out(dq, state.q)
+
+
+def _copy_back(dst, src_dev):
+    """Write a device result into the caller's array in place (numpy or tensor)."""
+    if _is_tensor(dst):
+        if dst.data_ptr() != src_dev.data_ptr():
+            dst.copy_(src_dev)
+    elif dst.flags.c_contiguous and dst.flags.writeable and dst.dtype.name == str(src_dev.dtype).split(".")[-1]:
+        import torch
+
+        torch.from_numpy(dst).copy_(src_dev)        # D2H straight into the caller's array
+    else:
+        dst[...] = src_dev.cpu().numpy()
+
+
+def _device_update(q_dev, res_dev, k_dev, a, b, dt):
+    lib = _lib.load()
+    import torch
+
+    dt_id = 0 if q_dev.dtype == torch.float32 else 1
+    _lib.check(lib.bbdg_lsrk_update(dt_id, q_dev.numel(), q_dev.data_ptr(), res_dev.data_ptr(), k_dev.data_ptr(),
+                                    float(a), float(b), float(dt), torch.cuda.current_stream().cuda_stream),
+               "bbdg_lsrk_update")
+
+
+def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorized", res=None) -> FieldState:
+    """One five-stage LSRK4 step, in place on state.q (reference solver.py:196-214).
+
+    A ``WaveSystem`` runs the five fused stage kernels on the device.  Any
+    other object with ``.rhs(state, lift_mode)`` (duck typing, as the
+    reference's own tests use) gets the stand-alone CUDA update kernel.
+    """
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    torch = _torch()
+    t0 = state.time
+    if isinstance(system, WaveSystem):
+        system._check(state)
+        lift = "dense" if system.basis == "nodal" else lift_mode
+        system._lift_id(lift)
+        q = system.to_device(state.q)
+        r = system.to_device(res) if res is not None else torch.empty_like(q)
+        tmp = torch.empty_like(q)
+        system.step_into(q, tmp, r, dt, lift)
+        _copy_back(state.q, q)
+        if res is not None:
+            _copy_back(res, r)
+        return FieldState(state.q, state.basis, t0 + dt)
+    # duck-typed system: host rhs, device update (no CPU arithmetic on the update)
+    host = not _is_tensor(state.q)
+    q = torch.from_numpy(np.ascontiguousarray(state.q)).cuda() if host else state.q
+    r = torch.zeros_like(q)
+    work = FieldState(state.q, state.basis, t0)
+    for s in range(5):
+        work.time = t0 + RK4C[s] * dt
+        k = system.rhs(work, lift_mode)
+        kd = torch.as_tensor(np.asarray(k) if not _is_tensor(k) else k).to(device=q.device, dtype=q.dtype)
+        _device_update(q, r, kd.contiguous(), RK4A[s], RK4B[s], dt)
+        if host:
+            state.q[...] = q.cpu().numpy()
+    if res is not None:
+        _copy_back(res, r)
+    return FieldState(state.q, state.basis, t0 + dt)
+
+
+def integrate(system, state: FieldState, dt: float, nsteps: int, lift_mode: str = "factorized", callback=None,
+              energy_guard: float | None = 10.0) -> FieldState:
+    """March nsteps with the state resident on the device (reference solver.py:217-239).
+
+    The five stages of each step ping-pong between two device buffers; the
+    host sees the state only for callbacks and the energy guard (every 20
+    steps), and the caller's array is updated in place at the end.
+    """
+    if not isinstance(system, WaveSystem):
+        res = np.zeros_like(state.q)
+        e0 = discrete_energy(system, state) if energy_guard else None
+        if callback:
+            callback(0, state)
+        for step in range(1, nsteps + 1):
+            state = lsrk4_step(system, state, dt, lift_mode, res)
+            if callback:
+                callback(step, state)
+        return state
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    system._check(state)
+    torch = _torch()
+    lift = "dense" if system.basis == "nodal" else lift_mode
+    system._lift_id(lift)
+    host = not _is_tensor(state.q)
+    bufs = [system.to_device(state.q), None]
+    bufs[1] = torch.empty_like(bufs[0])
+    res = torch.zeros_like(bufs[0])
+    cur = 0
+    e0 = discrete_energy(system, state) if energy_guard else None
+    if callback:
+        callback(0, state)
+    t = state.time
+    for step in range(1, nsteps + 1):
+        res.zero_()
+        for s in range(5):
+            system.stage_into(bufs[cur], bufs[cur ^ 1], res, RK4A[s], RK4B[s], dt, lift)
+            cur ^= 1
+        t = t + dt
+        if callback or (energy_guard and step % 20 == 0):
+            view = FieldState(bufs[cur], state.basis, t)
+            if callback:
+                cb_state = FieldState(bufs[cur].cpu().numpy(), state.basis, t) if host else view
+                callback(step, cb_state)
+            if energy_guard and step % 20 == 0:
+                e = discrete_energy(system, view)
+                if e > energy_guard * max(e0, 1e-300):
+                    _copy_back(state.q, bufs[cur])
+                    raise RuntimeError(f"unstable run: energy grew from {e0:.3e} to {e:.3e} by step {step}")
+    _copy_back(state.q, bufs[cur])
+    return FieldState(state.q, state.basis, t)
+
+
+def stable_dt(mesh: Mesh, N: int, c_max: float, cfl: float = 0.5) -> float:
+    """dt = cfl h_min / (c_max N^2) (reference solver.py:242-246)."""
+    if not 0.0 < cfl <= 1.0:
+        raise ValueError("cfl must lie in (0, 1]")
+    return cfl * mesh.h_min / (c_max * N * N)
+
+
+def exact_solution(xyz, tau: float):
+    """Standing wave on [-1/2,1/2]^3, rho = kappa = 1 (reference solver.py:249-261)."""
+    xyz = np.asarray(xyz)
+    cx, cy, cz = (np.cos(np.pi * xyz[..., i]) for i in range(3))
+    sx, sy, sz = (np.sin(np.pi * xyz[..., i]) for i in range(3))
+    p = cx * cy * cz * np.cos(_SQRT3 * np.pi * tau)
+    amp = np.sin(_SQRT3 * np.pi * tau) / _SQRT3
+    return p, np.stack([sx * cy * cz * amp, cx * sy * cz * amp, cx * cy * sz * amp])
+
+
+def initial_state(mesh: Mesh, N: int, basis: str, dtype=np.float64, node_kind: str = "warp_blend",
+                  tau: float = 0.0) -> FieldState:
+    """Nodal interpolation of the exact solution, converted in float64 (solver.py:264-279)."""
+    nops = NodalRefOps.build(N, node_kind)
+    p, u = exact_solution(mesh.map_reference_points(nops.nodes), tau)
+    q = np.stack([p, u[0], u[1], u[2]])
+    if basis == "bernstein":
+        q = nodal_to_bernstein(nops, q)
+    elif basis != "nodal":
+        raise ValueError(f"unknown basis {basis!r}")
+    return FieldState(q.astype(dtype), basis, tau)
+
+
+class ErrorFunctional:
+    """Quadrature of (p_h - p)^2 with a degree 2N+2 rule (solver.py:282-296)."""
+
+    def __init__(self, mesh: Mesh, ops):
+        pts, w = tet_rule(2 * ops.N + 2)
+        self.w = w
+        self.phys = mesh.map_reference_points(pts)
+        self.E = ops.eval_matrix(pts)
+        self.jac = mesh.jac
+
+    def __call__(self, state: FieldState) -> float:
+        q0 = state.q[0]
+        q0 = q0.double().cpu().numpy() if _is_tensor(q0) else np.asarray(q0, dtype=np.float64)
+        ph = q0 @ self.E.T
+        p, _ = exact_solution(self.phys, state.time)
+        return float(np.sqrt((((ph - p) ** 2) @ self.w) @ self.jac))
+
+
+def l2_error(system: WaveSystem, state: FieldState, functional: ErrorFunctional | None = None) -> float:
+    if functional is None:
+        functional = ErrorFunctional(system.mesh, system.ops_double)
+    return functional(state)
+
+
+def discrete_energy(system: WaveSystem, state: FieldState) -> float:
+    """sum_k J_k [p^T M p / kappa + rho sum_i u_i^T M u_i] (solver.py:306-312)."""
+    M = system.ops_double.mass
+    if _is_tensor(state.q):
+        torch = _torch()
+        q = state.q.double()
+        Md = torch.as_tensor(np.ascontiguousarray(M), device=q.device)
+        quad = torch.einsum("fkn,nm,fkm->fk", q, Md, q)
+        kap = torch.as_tensor(system.mat.kappa, device=q.device)
+        rho = torch.as_tensor(system.mat.rho, device=q.device)
+        jac = torch.as_tensor(system.mesh.jac, device=q.device)
+        return float(((quad[0] / kap + rho * quad[1:].sum(0)) * jac).sum())
+    q = np.asarray(state.q, dtype=np.float64)
+    quad = np.einsum("fkn,nm,fkm->fk", q, M, q)
+    return float(((quad[0] / system.mat.kappa + system.mat.rho * quad[1:].sum(axis=0)) * system.mesh.jac).sum())
+
+
+def _degree_from_block(Np: int) -> int:
+    N = 1
+    while (N + 1) * (N + 2) * (N + 3) // 6 < Np:
+        N += 1
+    if (N + 1) * (N + 2) * (N + 3) // 6 != Np:
+        raise ValueError(f"block length {Np} is not a tetrahedral space dimension")
+    return N
+
+
+def save_state(path, state: FieldState):
+    """One-line text header + raw (4,K,Np) bytes (reference solver.py:324-332)."""
+    q = state.q.cpu().numpy() if _is_tensor(state.q) else np.asarray(state.q)
+    header = (f"bbdg-state degree={_degree_from_block(q.shape[2])} K={q.shape[1]} "
+              f"basis={state.basis} precision={state.precision} time={state.time!r}\n")
+    with open(path, "wb") as fh:
+        fh.write(header.encode())
+        fh.write(np.ascontiguousarray(q).tobytes())
+
+
+def load_state(path) -> FieldState:
+    with open(path, "rb") as fh:
+        header = fh.readline().decode()
+        raw = fh.read()
+    fields = dict(tok.split("=") for tok in header.split()[1:])
+    N, K = int(fields["degree"]), int(fields["K"])
+    Np = (N + 1) * (N + 2) * (N + 3) // 6
+    dtype = np.float32 if fields["precision"] == "single" else np.float64
+    q = np.frombuffer(raw, dtype=dtype).reshape(4, K, Np).copy()
+    return FieldState(q, fields["basis"], float(fields["time"]))

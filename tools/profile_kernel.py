@@ -1,0 +1,52 @@
+"""Launch one hot-path kernel a few times for ncu (no timing printed -- numbers
+taken under a profiler are never bench values).
+
+    python tools/profile_kernel.py --N 9 --dtype f32 --op stage --lift optimal [--n 26] [--reps 3]
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=int, default=9)
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--op", default="stage", choices=["stage", "volume", "surface", "rhs", "update"])
+    ap.add_argument("--lift", default="optimal")
+    ap.add_argument("--basis", default="bernstein")
+    ap.add_argument("--n", type=int, default=26)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+
+    from paper_1512_06025_b200 import BernsteinRefOps, Materials, NodalRefOps, WaveSystem, cube_mesh
+    from paper_1512_06025_b200.solver import RK4A, RK4B, _device_update
+
+    m = cube_mesh(a.n)
+    ops = BernsteinRefOps.build(a.N) if a.basis == "bernstein" else NodalRefOps.build(a.N)
+    sy = WaveSystem(m, ops, Materials.homogeneous(m.K), dtype=np.float32 if a.dtype == "f32" else np.float64)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q = torch.randn((4, m.K, sy.Np), dtype=sy.torch_dtype, device="cuda", generator=g)
+    q2, res, rhs = torch.empty_like(q), torch.randn_like(q), torch.empty_like(q)
+    for _ in range(a.reps):
+        if a.op == "stage":
+            sy.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, a.lift)
+        elif a.op == "volume":
+            sy.volume_into(q, rhs)
+        elif a.op == "surface":
+            sy.surface_into(q, rhs, a.lift)
+        elif a.op == "rhs":
+            sy.rhs_into(q, rhs, a.lift)
+        else:
+            _device_update(q2, res, rhs, RK4A[1], RK4B[1], 1e-3)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()

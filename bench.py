@@ -96,7 +96,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -249,8 +249,12 @@ def run_ours(args, rank, world):
     Nd = dominant
     t_d = per_n[Nd] / args.steps
     ach = stage_bytes(Nd, s, K) / (t_d * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(args.dtype, {}).get(str(Nd))
     out["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                       "traffic": None, "kernel": f"tile_kernel<{args.dtype},N={Nd},OP_STAGE,{args.lift}>",
+                       "traffic": traffic, "kernel": f"tile_kernel<{args.dtype},N={Nd},OP_STAGE,{args.lift}>",
                        "peak_kind": peak_kind,
                        "bytes_per_launch": stage_bytes(Nd, s, K)}
     out["gpu_launches"] = args.steps * len(orders)
@@ -319,7 +323,7 @@ def main():
     ap.add_argument("--lift", default="optimal", choices=["optimal", "factorized", "dense"])
     ap.add_argument("--cpu-n", type=int, default=8, help="oracle sample mesh cube_mesh(cpu_n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--nodal", action="store_true", help="also time the nodal NPT comparison")
+    ap.add_argument("--no-nodal", dest="nodal", action="store_false", help="skip the nodal NPT comparison")
     ap.add_argument("--quick", action="store_true", help="skip the per-kernel breakdown")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -23,7 +23,7 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kThreads, L::total);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, L::threads, L::total);
     if (e != cudaSuccess) return set_cuda_error(e, "occupancy");
     if (b < 1) return set_error(BBDG_ERR_UNSUPPORTED, "tile kernel does not fit on an SM");
     blocks_per_sm = b;
@@ -31,8 +31,8 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
   const int64_t ntiles = (p.K + L::KE - 1) / L::KE;
   if (ntiles == 0) return BBDG_OK;
-  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms * blocks_per_sm);
-  kern<<<(unsigned)grid, kThreads, L::total, stream>>>(p);
+  const int64_t grid = std::min<int64_t>((ntiles + L::NG - 1) / L::NG, (int64_t)num_sms * blocks_per_sm);
+  kern<<<(unsigned)grid, L::threads, L::total, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "tile kernel launch");
 }
@@ -45,7 +45,7 @@ template <int OP, int LIFT, int BASIS> int64_t smem() { return Layout<BBDG_T, BB
 #define BBDG_CAT(a, b, c) BBDG_CAT_(a, b, c)
 
 KernelEntry BBDG_CAT(entry, BBDG_TNAME, BBDG_N)(int op, int lift, int basis) {
-  KernelEntry k{nullptr, nullptr, tile_elems<BBDG_N>(sizeof(BBDG_T))};
+  KernelEntry k{nullptr, nullptr, group_elems<BBDG_N>()};
 #define BBDG_CASE(O, Lf, B)                            \
   if (op == O && lift == Lf && basis == B) {           \
     k.launch = &launch<O, Lf, B>;                      \

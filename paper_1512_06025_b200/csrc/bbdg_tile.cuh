@@ -1,28 +1,26 @@
-// Element-tile kernels for the BB-DG (and nodal comparison) RHS + LSRK stage.
+// Element-group kernels for the BB-DG (and nodal comparison) RHS + LSRK stage.
 //
-// One persistent CTA loops over tiles of KE consecutive elements.  Each tile's
-// state block (4 fields x KE x Np, contiguous per field in the (4,K,Np) SoA
-// layout of reference solver.py:80-93), the LSRK register, the per-element
-// geometry and the compact face connectivity are staged into shared memory by
-// TMA bulk copies (cp.async.bulk + mbarrier), double-buffered so tile i+1
-// streams in while tile i computes.  All operator entries are index
-// arithmetic on the canonical multi-index order -- no operator tables are read
-// for the Bernstein volume, L0 or the optimal lift.
+// A persistent CTA holds NG independent *groups* of GW warps.  Each group owns
+// its own tiles (KE consecutive elements), its own double-buffered TMA staging
+// pipeline (cp.async.bulk + mbarrier) and work buffers, and synchronises only
+// with a named barrier (bar.sync 1+g, 32*GW); groups drift independently so one
+// group's barrier or shared-memory latency is hidden by the others.  The
+// closed-form stencil tables are built once per CTA and shared by the groups.
 //
-// Phases (each a strided loop over the tile's work items, __syncthreads
-// between phases):
-//   S1  upwind flux at every face point (own trace from smem, neighbour trace
-//       gathered from global / halo)                 reference solver.py:166-184
-//   S2  L0 per face (<=7 nnz/row, closed form)       reference bernstein.py:221-229
-//   S3  lift: optimal = N one-degree reduction sweeps (Alg. 1,
+// Per tile and group (reference solver.py:139-214):
+//   S1  upwind flux at every face point: own trace from smem, neighbour trace
+//       gathered from L2 / the halo buffer               (solver.py:166-184)
+//   S2  L0 on each face, <=7 closed-form lanes              (bernstein.py:221-229)
+//   S3  lift: optimal = N one-degree reduction sweeps per face (Alg. 1,
 //       bernstein.py:313-329); factorized = E_L ELL rows (bernstein.py:301-310);
-//       dense = M^{-1}M^f rows (bernstein.py:332-347 / nodal.py:236-241)
-//   V1  BB volume, degree N-1 half: Delta_m = q[b+e_{m+1}] - q[b+e_0] for all 4
-//       fields, contracted with the geometric factors in place
-//   V2  BB volume, degree N half: one-degree elevation (4 nnz/row) of V1's
-//       result.  V1+V2 equal reference volume_rhs (solver.py:139-158,
-//       bernstein.py:436-444) up to rounding; constant states give exactly 0.
-//   EP  epilogue: rhs / rhs accumulate / fused LSRK stage (solver.py:208-213)
+//       dense = M^{-1}M^f rows (bernstein.py:332-347, nodal.py:236-241)
+//       S1-S3 are warp-local (one warp owns whole faces): __syncwarp only.
+//   V1  volume, degree N-1 half: Delta_m = q[b+e_{m+1}] - q[b+e_0] (4 fields)
+//       contracted with the geometric factors
+//   V2  volume, degree N half: one-degree elevation (4 lanes).  V1+V2 equal
+//       volume_rhs (solver.py:139-158, bernstein.py:436-444) up to rounding and
+//       give exactly 0 on constant states.
+//   EP  rhs store / accumulate, or the fused LSRK stage (solver.py:211-213).
 #pragma once
 #include <type_traits>
 
@@ -34,7 +32,6 @@ enum Op : int { OP_VOLUME = 0, OP_SURFACE = 1, OP_RHS = 2, OP_STAGE = 3 };
 enum Lift : int { LIFT_FACTORIZED = 0, LIFT_OPTIMAL = 1, LIFT_DENSE = 2 };
 enum Basis : int { BASIS_BERNSTEIN = 0, BASIS_NODAL = 1 };
 
-constexpr int kThreads = 256;
 constexpr int kGeoVol = 12;   // rst_dx[m][i] (9), kappa, inv_rho, pad
 constexpr int kGeoSurf = 24;  // per face: n0 n1 n2 face_scale tau_p tau_u
 
@@ -82,29 +79,41 @@ __host__ __device__ constexpr int layer_off(int N, int j) {
   for (int jj = 0; jj < j; ++jj) o += tri_dim(N - jj);
   return o;
 }
+__host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
+__host__ __device__ constexpr int odd_up(int n) { return n | 1; }
 
-template <int N> __host__ __device__ constexpr int tile_elems(int sz) {
-  // ~384 nodes per tile, KE*Np*sz a multiple of 16 B (TMA bulk granularity)
-  int ke = (384 + Dims<N>::Np - 1) / Dims<N>::Np;
-  while ((ke * Dims<N>::Np * sz) % 16 != 0) ++ke;
-  return ke;
+// group geometry per degree: elements per group tile (~120..250 nodes) and warps
+// per group; face pairs per warp = 4 KE / GW
+template <int N> __host__ __device__ constexpr int group_elems() {
+  constexpr int ke[10] = {0, 32, 12, 6, 7, 4, 3, 2, 2, 1};
+  return ke[N];
+}
+template <int N> __host__ __device__ constexpr int group_warps() {
+  constexpr int gw[10] = {0, 4, 4, 4, 4, 4, 4, 4, 4, 4};
+  return gw[N];
 }
 
-__host__ __device__ constexpr int align16(int b) { return (b + 15) & ~15; }
-__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
-
-// Shared-memory layout of one CTA.
+// ----------------------------------------------------------------------------
+// shared-memory layout
+// ----------------------------------------------------------------------------
 template <typename T, int N, int OP, int LIFT, int BASIS> struct Layout {
   using D = Dims<N>;
   static constexpr int Np = D::Np, Nfp = D::Nfp, Npm = D::Npm;
-  static constexpr int KE = tile_elems<N>(sizeof(T));
+  static constexpr int KE = group_elems<N>();
+  static constexpr int GW = group_warps<N>();
+  static constexpr int GT = 32 * GW;
+  static constexpr int PPW = 4 * KE / GW;    // face pairs per warp
+  static_assert((4 * KE) % GW == 0, "face pairs must split evenly over the group's warps");
   static constexpr int sz = (int)sizeof(T);
+  static constexpr int NPS = odd_up(Np);     // padded per-face strides: odd -> no bank aliasing
+  static constexpr int NFS = odd_up(Nfp);
   static constexpr bool VOL = OP != OP_SURFACE;
   static constexpr bool SURF = OP != OP_VOLUME;
+  static constexpr bool RES = OP == OP_STAGE;
   static constexpr bool BB = BASIS == BASIS_BERNSTEIN;
   static constexpr bool OPT = SURF && BB && LIFT == LIFT_OPTIMAL;
   static constexpr bool FAC = SURF && BB && LIFT == LIFT_FACTORIZED;
-  // index / coefficient tables (closed forms, built once per CTA)
+  // CTA-wide tables (closed forms, built once)
   static constexpr int o_v2par = 0;                                    // ushort4 [Np]  parents in P_{N-1}
   static constexpr int o_v2coef = align16(o_v2par + 8 * Np);           // V4<T>  [Np]  alpha_j
   static constexpr int o_v1chl = align16(o_v2coef + 4 * sz * Np);      // ushort4 [Npm] children in P_N
@@ -115,39 +124,40 @@ template <typename T, int N, int OP, int LIFT, int BASIS> struct Layout {
   static constexpr int o_cpos = align16(o_l0val + 8 * sz * Nfp);       // ushort4 [Npm]
   static constexpr int o_ccoef = align16(o_cpos + 8 * Npm);            // V4<T> [Npm]
   static constexpr int o_lidx = align16(o_ccoef + 4 * sz * Npm);       // ushort4 [Np]
-  static constexpr int o_bar = align16(o_lidx + 8 * Np);               // 3 x mbarrier (2 stages + res)
-  // staging (two buffers)
-  static constexpr int b_q = 4 * KE * Np * sz;
-  static constexpr int b_gv = KE * kGeoVol * sz;
-  static constexpr int b_gs = SURF ? KE * kGeoSurf * sz : 0;
-  static constexpr int b_nbr = SURF ? KE * 16 : 0;
-  static constexpr int b_code = SURF ? KE * 4 : 0;
+  static constexpr int tables = align16(o_lidx + 8 * Np);
+  // per-group block.  Staged chunks get 32 B slack: TMA copies the 16-byte
+  // aligned window around each chunk and the consumer offsets its pointer.
+  static constexpr int cq = align16(KE * Np * sz) + 32;
+  static constexpr int cgv = align16(KE * kGeoVol * sz) + 32;
+  static constexpr int cgs = SURF ? align16(KE * kGeoSurf * sz) + 32 : 0;
+  static constexpr int cnb = SURF ? KE * 16 + 32 : 0;
+  static constexpr int ccd = SURF ? align16(KE * 4) + 32 : 0;
   static constexpr int s_q = 0;
-  static constexpr int s_gv = align16(s_q + b_q);
-  static constexpr int s_gs = align16(s_gv + b_gv);
-  static constexpr int s_nbr = align16(s_gs + b_gs);
-  static constexpr int s_code = align16(s_nbr + b_nbr);
-  static constexpr int stage_bytes = align16(s_code + b_code);
-  static constexpr int o_rest = o_bar + 24;                            // 2 x u32 fallback masks
-  static constexpr int o_stage = align16(o_rest + 8);
-  // LSRK register tile (OP_STAGE): single buffer, bulk-copied at tile start, read by the epilogue
-  static constexpr bool RES = OP == OP_STAGE;
-  static constexpr int b_res = RES ? 4 * KE * Np * sz : 0;
-  static constexpr int o_res = o_stage + 2 * stage_bytes;
-  // work buffers: flux (S1) -> lift input (S2) -> W (cascade, layer-major per face);
-  // the V1 buffer reuses the flux region (dead after S2, barrier in between)
-  static constexpr int o_work = align16(o_res + b_res);
-  static constexpr int n_flux = SURF ? 2 * KE * 4 * Nfp : 0;
+  static constexpr int s_gv = 4 * cq;
+  static constexpr int s_gs = s_gv + cgv;
+  static constexpr int s_nbr = s_gs + cgs;
+  static constexpr int s_code = s_nbr + cnb;
+  static constexpr int stage_bytes = s_code + ccd;
+  static constexpr int g_res = 2 * stage_bytes;
+  static constexpr int g_flux = g_res + (RES ? 4 * cq : 0);
+  static constexpr int n_flux = SURF ? 2 * KE * 4 * NFS : 0;
+  static constexpr int g_vq = align16(g_flux + n_flux * sz);
   static constexpr int n_vq = (SURF && !OPT) ? 4 * KE * 4 * Nfp : 0;
-  static constexpr int n_W = OPT ? 2 * KE * 4 * Np : 0;
+  static constexpr int g_W = align16(g_vq + n_vq * sz);
+  static constexpr int n_W = OPT ? 2 * KE * 4 * NPS : 0;
+  static constexpr int g_w = align16(g_W + n_W * sz);
   static constexpr int n_w = (VOL && BB) ? 4 * KE * Npm : 0;
-  static constexpr int o_flux = o_work;
-  static constexpr int o_vq = align16(o_flux + n_flux * sz);
-  static constexpr int o_W = align16(o_vq + n_vq * sz);
-  static constexpr int end_main = align16(o_W + n_W * sz);
-  static constexpr bool W_ALIAS = n_w <= n_flux;
-  static constexpr int o_w = W_ALIAS ? o_flux : end_main;
-  static constexpr int total = W_ALIAS ? end_main : align16(end_main + n_w * sz);
+  static constexpr int g_bar = align16(g_w + n_w * sz);                // 3 mbarriers + 3 fallback masks
+  static constexpr int group_bytes = align16(g_bar + 40);
+  // groups per CTA: one CTA per SM with up to 1024 threads, so the tables exist once per SM
+  static constexpr int ng_fit(int budget) {
+    for (int n = 1024 / GT; n >= 1; --n)
+      if (tables + n * group_bytes <= budget) return n;
+    return 0;
+  }
+  static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
+  static constexpr int threads = NG * GT;
+  static constexpr int total = tables + NG * group_bytes;
 };
 
 // ----------------------------------------------------------------------------
@@ -168,7 +178,7 @@ __device__ __forceinline__ void decode2(int M, int i, int& b0, int& b1) {
   b1 = r;
 }
 
-template <typename T, int N, class L> __device__ void build_tables(unsigned char* sm) {
+template <typename T, int N, class L> __device__ void build_tables(unsigned char* sm, int tid, int nthreads) {
   constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm;
   ushort4* v2par = reinterpret_cast<ushort4*>(sm + L::o_v2par);
   V4<T>* v2coef = reinterpret_cast<V4<T>*>(sm + L::o_v2coef);
@@ -180,8 +190,7 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
   ushort4* cpos = reinterpret_cast<ushort4*>(sm + L::o_cpos);
   V4<T>* ccoef = reinterpret_cast<V4<T>*>(sm + L::o_ccoef);
   ushort4* lidx = reinterpret_cast<ushort4*>(sm + L::o_lidx);
-  const int tid = threadIdx.x;
-  for (int i = tid; i < Np; i += kThreads) {
+  for (int i = tid; i < Np; i += nthreads) {
     int a0, a1, a2;
     decode3(N, i, a0, a1, a2);
     const int a[4] = {a0, a1, a2, N - a0 - a1 - a2};
@@ -199,13 +208,13 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
     }
     lidx[i] = make_ushort4(li[0], li[1], li[2], li[3]);
   }
-  for (int i = tid; i < Npm; i += kThreads) {
+  for (int i = tid; i < Npm; i += nthreads) {
     int b0, b1, b2;
     decode3(N - 1, i, b0, b1, b2);
     v1chl[i] = make_ushort4(pos3(N, b0 + 1, b1, b2), pos3(N, b0, b1 + 1, b2), pos3(N, b0, b1, b2 + 1),
                             pos3(N, b0, b1, b2));
   }
-  for (int m = tid; m < Nfp; m += kThreads) {
+  for (int m = tid; m < Nfp; m += nthreads) {
     int b0, b1;
     decode2(N, m, b0, b1);
     const int b[3] = {b0, b1, N - b0 - b1};
@@ -230,24 +239,22 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
     for (int j = 0; j < 3; ++j)
       for (int k = 0; k < 3; ++k) {
         if (j == k) continue;
-        int g[3] = {b[0], b[1], b[2]};
-        g[j] += 1;
-        g[k] -= 1;
+        int gg[3] = {b[0], b[1], b[2]};
+        gg[j] += 1;
+        gg[k] -= 1;
         const bool ok = b[k] >= 1;
-        pp[l] = ok ? pos2(N, g[0], g[1]) : m;
+        pp[l] = ok ? pos2(N, gg[0], gg[1]) : m;
         cv[l] = ok ? T(0.5 * double((b[j] + 1) * b[k])) : T(0);
         ++l;
       }
-    pp[7] = m;
-    cv[7] = T(0);
     l0pos[2 * m] = make_ushort4(pp[1], pp[2], pp[3], pp[4]);
     l0pos[2 * m + 1] = make_ushort4(pp[5], pp[6], 0, 0);
     l0val[2 * m] = V4<T>{cv[0], cv[1], cv[2], cv[3]};
     l0val[2 * m + 1] = V4<T>{cv[4], cv[5], cv[6], T(0)};
   }
   // cascade item (target degree ml, point b): children b+e_k in degree ml+1, coefficients
-  // (b_k+1)/(ml+1) * ell_j/ell_{j-1} (j = N - ml), so the buffer holds ell-scaled layers
-  for (int t = tid; t < Npm; t += kThreads) {
+  // (b_k+1)/(ml+1) * ell_j/ell_{j-1} (j = N - ml): the buffer holds ell-scaled layers
+  for (int t = tid; t < Npm; t += nthreads) {
     int r = t, ml = 0;
     while (r >= tri_dim(ml)) { r -= tri_dim(ml); ++ml; }
     int b0, b1;
@@ -260,93 +267,90 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
 }
 
 // ----------------------------------------------------------------------------
-// staging: which chunks go through TMA, which through plain loads
+// staging: TMA bulk copies of 16-byte aligned windows, cooperative fallback
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ bool tma_ok(const void* src, uint32_t bytes) {
-  return ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((bytes & 15) == 0) && bytes > 0;
-}
-
-template <typename T, int N, class L> struct Chunk {
-  const void* src;
-  int dst;  // byte offset within the stage buffer
+struct Chunk {
+  const unsigned char* src;  // first byte the tile needs
+  const unsigned char* end;  // end of the source array (the window must stay inside)
+  int dst;                   // chunk base offset (16-aligned) from the group block
   uint32_t bytes;
 };
 
-template <typename T, int N, class L>
-__device__ __forceinline__ int tile_chunks(const Params<T>& p, int64_t k0, int nv, Chunk<T, N, L>* c) {
+__device__ __forceinline__ int win_off(const void* p) { return (int)(reinterpret_cast<uintptr_t>(p) & 15); }
+__device__ __forceinline__ uint32_t win_len(const Chunk& c) {
+  return (uint32_t)((reinterpret_cast<uintptr_t>(c.src) & 15) + c.bytes + 15) & ~15u;
+}
+__device__ __forceinline__ bool window_ok(const Chunk& c) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(c.src) & ~uintptr_t(15);
+  return c.bytes > 0 && (reinterpret_cast<uintptr_t>(c.src) & 3) == 0 &&
+         a + win_len(c) <= reinterpret_cast<uintptr_t>(c.end);
+}
+
+template <typename T, class L>
+__device__ __forceinline__ int tile_chunks(const Params<T>& p, int64_t k0, int nv, int base, Chunk* c) {
   constexpr int Np = L::Np;
-  int n = 0;
   const int64_t fs = p.K * Np;
+  const unsigned char* qend = reinterpret_cast<const unsigned char*>(p.q + 4 * fs);
+  int n = 0;
   for (int F = 0; F < 4; ++F)
-    c[n++] = {p.q + F * fs + k0 * Np, L::s_q + F * L::KE * Np * (int)sizeof(T), (uint32_t)(nv * Np * sizeof(T))};
-  c[n++] = {p.geo_vol + k0 * kGeoVol, L::s_gv, (uint32_t)(nv * kGeoVol * sizeof(T))};
+    c[n++] = {reinterpret_cast<const unsigned char*>(p.q + F * fs + k0 * Np), qend, base + L::s_q + F * L::cq,
+              (uint32_t)(nv * Np * sizeof(T))};
+  c[n++] = {reinterpret_cast<const unsigned char*>(p.geo_vol + k0 * kGeoVol),
+            reinterpret_cast<const unsigned char*>(p.geo_vol + p.K * kGeoVol), base + L::s_gv,
+            (uint32_t)(nv * kGeoVol * sizeof(T))};
   if constexpr (L::SURF) {
-    c[n++] = {p.geo_surf + k0 * kGeoSurf, L::s_gs, (uint32_t)(nv * kGeoSurf * sizeof(T))};
-    c[n++] = {p.nbr + k0 * 4, L::s_nbr, (uint32_t)(nv * 16)};
-    c[n++] = {p.code + k0, L::s_code, (uint32_t)(nv * 4)};
+    c[n++] = {reinterpret_cast<const unsigned char*>(p.geo_surf + k0 * kGeoSurf),
+              reinterpret_cast<const unsigned char*>(p.geo_surf + p.K * kGeoSurf), base + L::s_gs,
+              (uint32_t)(nv * kGeoSurf * sizeof(T))};
+    c[n++] = {reinterpret_cast<const unsigned char*>(p.nbr + k0 * 4),
+              reinterpret_cast<const unsigned char*>(p.nbr + p.K * 4), base + L::s_nbr, (uint32_t)(nv * 16)};
+    c[n++] = {reinterpret_cast<const unsigned char*>(p.code + k0),
+              reinterpret_cast<const unsigned char*>(p.code + p.K), base + L::s_code, (uint32_t)(nv * 4)};
   }
   return n;
 }
 
-// producer (one thread): bulk-copy every TMA-able chunk; returns the bitmask of
-// chunks left for the cooperative fallback
-template <typename T, int N, class L>
-__device__ uint32_t issue_tile(const Params<T>& p, int64_t k0, int nv, unsigned char* stage, uint64_t* bar) {
-  Chunk<T, N, L> c[8];
-  const int n = tile_chunks<T, N, L>(p, k0, nv, c);
+// producer (one thread): window copies of every chunk that allows it; returns the
+// bitmask of chunks left for the cooperative fallback.  Always arrives once.
+__device__ __forceinline__ uint32_t issue_chunks(const Chunk* c, int n, unsigned char* gbase, uint64_t* bar) {
   uint32_t bytes = 0, rest = 0;
   for (int i = 0; i < n; ++i) {
-    if (tma_ok(c[i].src, c[i].bytes)) bytes += c[i].bytes;
+    if (window_ok(c[i])) bytes += win_len(c[i]);
     else rest |= 1u << i;
   }
   mbar_expect_tx(bar, bytes);
-  for (int i = 0; i < n; ++i)
-    if (!((rest >> i) & 1)) tma_bulk_g2s(stage + c[i].dst, c[i].src, c[i].bytes, bar);
+  for (int i = 0; i < n; ++i) {
+    if ((rest >> i) & 1) continue;
+    const void* a = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(c[i].src) & ~uintptr_t(15));
+    tma_bulk_g2s(gbase + c[i].dst, a, win_len(c[i]), bar);
+  }
   return rest;
 }
 
-// cooperative fallback for chunks TMA cannot take (unaligned field bases, odd tails)
-template <typename T, int N, class L>
-__device__ void finish_tile(const Params<T>& p, int64_t k0, int nv, unsigned char* stage, uint32_t rest) {
-  Chunk<T, N, L> c[8];
-  const int n = tile_chunks<T, N, L>(p, k0, nv, c);
+template <int GT>
+__device__ __forceinline__ void fallback_chunks(const Chunk* c, int n, unsigned char* gbase, uint32_t rest,
+                                                int gtid) {
   for (int i = 0; i < n; ++i) {
     if (!((rest >> i) & 1)) continue;
     const uint32_t words = c[i].bytes / 4;
-    const uint32_t* s = static_cast<const uint32_t*>(c[i].src);
-    uint32_t* d = reinterpret_cast<uint32_t*>(stage + c[i].dst);
-    for (uint32_t w = threadIdx.x; w < words; w += kThreads) d[w] = __ldg(s + w);
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(c[i].src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(gbase + c[i].dst + win_off(c[i].src));
+    for (uint32_t w = gtid; w < words; w += GT) d[w] = __ldg(s + w);
   }
 }
 
-// ----------------------------------------------------------------------------
-// the tile kernel
-// ----------------------------------------------------------------------------
-template <typename T> __device__ __forceinline__ void load6(const T* g, T* v) {
-  // 6 contiguous values, 8-byte aligned (fp32) / 16-byte aligned (fp64)
-  if constexpr (sizeof(T) == 4) {
-    const float2* g2 = reinterpret_cast<const float2*>(g);
-    const float2 a = g2[0], b = g2[1], c = g2[2];
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
-  } else {
-    const double2* g2 = reinterpret_cast<const double2*>(g);
-    const double2 a = g2[0], b = g2[1], c = g2[2];
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
-  }
-}
-template <typename T> __device__ __forceinline__ void load12(const T* g, T* v) {
-  const V4<T>* g4 = reinterpret_cast<const V4<T>*>(g);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const V4<T> x = g4[i];
-    v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
-  }
+template <int GT> __device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(g + 1), "n"(GT) : "memory");
 }
 
+// ----------------------------------------------------------------------------
+// the kernel
+// ----------------------------------------------------------------------------
 template <typename T, int N, int OP, int LIFT, int BASIS>
-__global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
+__global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) tile_kernel(const Params<T> p) {
   using L = Layout<T, N, OP, LIFT, BASIS>;
-  constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm, KE = L::KE;
+  constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm, KE = L::KE, NG = L::NG;
+  constexpr int NPS = L::NPS, NFS = L::NFS, GT = L::GT;
   extern __shared__ __align__(128) unsigned char sm[];
 
   const ushort4* v2par = reinterpret_cast<const ushort4*>(sm + L::o_v2par);
@@ -359,15 +363,21 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
   const ushort4* cpos = reinterpret_cast<const ushort4*>(sm + L::o_cpos);
   const V4<T>* ccoef = reinterpret_cast<const V4<T>*>(sm + L::o_ccoef);
   const ushort4* lidx = reinterpret_cast<const ushort4*>(sm + L::o_lidx);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::o_bar);
-  T* sflux = reinterpret_cast<T*>(sm + L::o_flux);   // [g][e][f][Nfp]
-  T* svq = reinterpret_cast<T*>(sm + L::o_vq);       // [F][e][4 Nfp]
-  T* sW = reinterpret_cast<T*>(sm + L::o_W);         // [g][e][f][Np] layer-major, ell-scaled
-  T* sw = reinterpret_cast<T*>(sm + L::o_w);         // [F][e][Npm]
 
   const int tid = threadIdx.x;
-  build_tables<T, N, L>(sm);
-  if (tid == 0) {
+  const int g = tid / GT;            // group
+  const int gtid = tid - g * GT;     // thread within the group
+  const int wg = gtid >> 5, lane = gtid & 31;
+  unsigned char* gb = sm + L::tables + g * L::group_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gb + L::g_bar);   // [0,1] stages, [2] res
+  uint32_t* rest = reinterpret_cast<uint32_t*>(gb + L::g_bar + 24);
+  T* sflux = reinterpret_cast<T*>(gb + L::g_flux);   // [grp][ef][NFS]
+  T* svq = reinterpret_cast<T*>(gb + L::g_vq);       // [F][e][4 Nfp]
+  T* sW = reinterpret_cast<T*>(gb + L::g_W);         // [grp][ef][NPS] layer-major, ell-scaled
+  T* sw = reinterpret_cast<T*>(gb + L::g_w);         // [F][e][Npm]
+
+  build_tables<T, N, L>(sm, tid, L::threads);
+  if (gtid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);
@@ -377,80 +387,74 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
 
   const int64_t ntiles = (p.K + KE - 1) / KE;
   const int64_t fs = p.K * Np;
-  // the TMA path covers every chunk when the field planes are 16-byte aligned; then
-  // only a short last tile can need the cooperative fallback
-  const bool planes_aligned = ((fs * (int64_t)sizeof(T)) & 15) == 0 &&
-                              ((reinterpret_cast<uintptr_t>(p.q) | reinterpret_cast<uintptr_t>(p.res)) & 15) == 0;
-  T* sres = reinterpret_cast<T*>(sm + L::o_res);     // [F][e][Np]
-  uint32_t* rest = reinterpret_cast<uint32_t*>(sm + L::o_rest);
-  int64_t tile = blockIdx.x;
-  if (tid == 0 && tile < ntiles) {
-    const int64_t k0 = tile * KE;
-    rest[0] = issue_tile<T, N, L>(p, k0, (int)(p.K - k0 < KE ? p.K - k0 : KE), sm + L::o_stage, &bars[0]);
-  }
-  __syncthreads();
-
-  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it & 1;
-    unsigned char* stage = sm + L::o_stage + st * L::stage_bytes;
+  const int64_t stride = (int64_t)gridDim.x * NG;
+  int64_t tile = (int64_t)blockIdx.x * NG + g;
+  Chunk ch[8];
+  if (gtid == 0 && tile < ntiles) {
     const int64_t k0 = tile * KE;
     const int nv = (int)(p.K - k0 < KE ? p.K - k0 : KE);
-    // prefetch the next tile into the other buffer (freed by the previous iteration's barrier)
-    const int64_t nt = tile + gridDim.x;
-    if (tid == 0 && nt < ntiles) {
+    const int n = tile_chunks<T, L>(p, k0, nv, 0, ch);
+    rest[0] = issue_chunks(ch, n, gb, &bars[0]);
+  }
+  group_sync<GT>(g);
+
+  for (int it = 0; tile < ntiles; tile += stride, ++it) {
+    const int st = it & 1;
+    unsigned char* stage = gb + st * L::stage_bytes;
+    const int64_t k0 = tile * KE;
+    const int nv = (int)(p.K - k0 < KE ? p.K - k0 : KE);
+    // producer: next tile into the other stage buffer (freed by the last group barrier),
+    // this tile's LSRK register into the res buffer (consumed by the epilogue)
+    const int64_t nt = tile + stride;
+    if (gtid == 0) {
       fence_proxy_async();
-      const int64_t k1 = nt * KE;
-      rest[st ^ 1] = issue_tile<T, N, L>(p, k1, (int)(p.K - k1 < KE ? p.K - k1 : KE),
-                                         sm + L::o_stage + (st ^ 1) * L::stage_bytes, &bars[st ^ 1]);
-    }
-    // this tile's LSRK register: one bulk copy per field into the single res buffer
-    // (freed by the previous iteration's final barrier); consumed by the epilogue
-    const bool res_tma = L::RES && planes_aligned && ((nv * Np * (int)sizeof(T)) & 15) == 0;
-    if constexpr (L::RES) {
-      if (tid == 0 && res_tma) {
-        fence_proxy_async();
-        mbar_expect_tx(&bars[2], 4u * nv * Np * sizeof(T));
-#pragma unroll
+      if (nt < ntiles) {
+        const int64_t k1 = nt * KE;
+        const int nv1 = (int)(p.K - k1 < KE ? p.K - k1 : KE);
+        const int n = tile_chunks<T, L>(p, k1, nv1, (st ^ 1) * L::stage_bytes, ch);
+        rest[st ^ 1] = issue_chunks(ch, n, gb, &bars[st ^ 1]);
+      }
+      if constexpr (L::RES) {
+        const unsigned char* rend = reinterpret_cast<const unsigned char*>(p.res + 4 * fs);
+        Chunk rc[4];
         for (int F = 0; F < 4; ++F)
-          tma_bulk_g2s(sres + F * KE * Np, p.res + F * fs + k0 * Np, nv * Np * sizeof(T), &bars[2]);
+          rc[F] = {reinterpret_cast<const unsigned char*>(p.res + F * fs + k0 * Np), rend, L::g_res + F * L::cq,
+                   (uint32_t)(nv * Np * sizeof(T))};
+        rest[2] = issue_chunks(rc, 4, gb, &bars[2]);
       }
     }
     mbar_wait(&bars[st], (it >> 1) & 1);
-    const uint32_t rmask = rest[st];   // written one iteration ago, behind a CTA barrier
-    if (rmask) finish_tile<T, N, L>(p, k0, nv, stage, rmask);
-    __syncthreads();
+    const uint32_t rmask = rest[st];   // written one iteration ago, behind a group barrier
+    if (rmask) {
+      const int n = tile_chunks<T, L>(p, k0, nv, st * L::stage_bytes, ch);
+      fallback_chunks<GT>(ch, n, gb, rmask, gtid);
+      group_sync<GT>(g);
+    }
 
-    const T* sq = reinterpret_cast<const T*>(stage + L::s_q);          // [F][e][Np]
-    const T* sgv = reinterpret_cast<const T*>(stage + L::s_gv);         // [e][12]
-    const T* sgs = reinterpret_cast<const T*>(stage + L::s_gs);         // [e][4][6]
-    const int32_t* snbr = reinterpret_cast<const int32_t*>(stage + L::s_nbr);
-    const int32_t* scode = reinterpret_cast<const int32_t*>(stage + L::s_code);
+    // staged views (each chunk starts at its 16-byte window offset)
+    const T* sq[4];
+#pragma unroll
+    for (int F = 0; F < 4; ++F)
+      sq[F] = reinterpret_cast<const T*>(stage + L::s_q + F * L::cq + win_off(p.q + F * fs + k0 * Np));
+    const T* sgv = reinterpret_cast<const T*>(stage + L::s_gv + win_off(p.geo_vol + k0 * kGeoVol));
+    const T* sgs = reinterpret_cast<const T*>(stage + L::s_gs + win_off(p.geo_surf + k0 * kGeoSurf));
+    const int32_t* snbr = reinterpret_cast<const int32_t*>(stage + L::s_nbr + win_off(p.nbr + k0 * 4));
+    const int32_t* scode = reinterpret_cast<const int32_t*>(stage + L::s_code + win_off(p.code + k0));
 
-    constexpr int EP_ITEMS = (KE * Np + kThreads - 1) / kThreads;
-    T* outF = p.out + k0 * Np;
-    T* resF = p.res + k0 * Np;
-
-    // ------------------------------------------------------------- surface
-    // Warp-local pipeline: face pair ef = e*4+f belongs to warp (ef % 8); flux (S1),
-    // L0 (S2) and the cascade (S3) of a face only touch that face's data, so the
-    // phases are separated by __syncwarp, not CTA barriers.
+    // ------------------------------------------------------------- surface (warp-local)
     if constexpr (L::SURF) {
       constexpr int NPAIR = KE * 4;
-      constexpr int NW = kThreads / 32;
-      constexpr int PPW = (NPAIR + NW - 1) / NW;  // face pairs per warp
-      const int warp = tid >> 5, lane = tid & 31;
-      // S1: upwind flux at every face point (reference solver.py:170-184)
-      for (int it = lane; it < PPW * Nfp; it += 32) {
-        const int pw = it / Nfp, m = it - pw * Nfp;
-        const int ef = warp * PPW + pw;
-        if (ef >= NPAIR) continue;
-        const int e = ef >> 2, f = ef & 3, fm = f * Nfp + m;
-        T g[6];
-        load6(sgs + e * kGeoSurf + f * 6, g);
+      constexpr int PPW = L::PPW;             // face pairs per warp: warp wg owns ef in [wg*PPW, wg*PPW+PPW)
+      // S1: upwind flux at every face point of the warp's faces (reference solver.py:170-184)
+      for (int i = lane; i < PPW * Nfp; i += 32) {
+        const int pw = i / Nfp, m = i - pw * Nfp;
+        const int ef = wg * PPW + pw;
+        const int e = ef >> 2, f = ef & 3;
+        const T* gsf = sgs + e * kGeoSurf + f * 6;
         const int pos = trace[f * Nfp + m];
         T loc[4], nb[4];
 #pragma unroll
-        for (int F = 0; F < 4; ++F) loc[F] = sq[(F * KE + e) * Np + pos];
+        for (int F = 0; F < 4; ++F) loc[F] = sq[F][e * Np + pos];
         const int cd = (scode[e] >> (8 * f)) & 0xff;
         const bool bnd = (cd >> 5) & 1;
         if (bnd || e >= nv) {
@@ -472,22 +476,20 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
         }
         const T j1 = nb[1] - loc[1], j2 = nb[2] - loc[2], j3 = nb[3] - loc[3];
         const T jp = bnd ? T(-2) * loc[0] : nb[0] - loc[0];
-        const T jun = g[0] * j1 + g[1] * j2 + g[2] * j3;
+        const T jun = gsf[0] * j1 + gsf[1] * j2 + gsf[2] * j3;
         const T half = T(0.5);
-        sflux[e * 4 * Nfp + fm] = half * (g[4] * jp - jun) * g[3];
-        sflux[(KE + e) * 4 * Nfp + fm] = half * (g[5] * jun - jp) * g[3];
+        sflux[ef * NFS + m] = half * (gsf[4] * jp - jun) * gsf[3];
+        sflux[(NPAIR + ef) * NFS + m] = half * (gsf[5] * jun - jp) * gsf[3];
       }
       __syncwarp();
 
       if constexpr (L::BB && LIFT != LIFT_DENSE) {
         // S2: L0 on the warp's faces, both field groups (closed-form 7-lane rows)
-        for (int it = lane; it < PPW * Nfp; it += 32) {
-          const int pw = it / Nfp, m = it - pw * Nfp;
-          const int ef = warp * PPW + pw;
-          if (ef >= NPAIR) continue;
-          const int e = ef >> 2, f = ef & 3, fm = f * Nfp + m;
-          const T* Fp = sflux + e * 4 * Nfp + f * Nfp;
-          const T* Fu = Fp + KE * 4 * Nfp;
+        for (int i = lane; i < PPW * Nfp; i += 32) {
+          const int pw = i / Nfp, m = i - pw * Nfp;
+          const int ef = wg * PPW + pw;
+          const T* Fp = sflux + ef * NFS;
+          const T* Fu = sflux + (NPAIR + ef) * NFS;
           const ushort4 pa = l0pos[2 * m], pb = l0pos[2 * m + 1];
           const V4<T> ca = l0val[2 * m], cb = l0val[2 * m + 1];
           const T vp = ca.x * Fp[m] + ca.y * Fp[pa.x] + ca.z * Fp[pa.y] + ca.w * Fp[pa.z] + cb.x * Fp[pa.w] +
@@ -495,15 +497,15 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
           const T vu = ca.x * Fu[m] + ca.y * Fu[pa.x] + ca.z * Fu[pa.y] + ca.w * Fu[pa.z] + cb.x * Fu[pa.w] +
                        cb.y * Fu[pb.x] + cb.z * Fu[pb.y];
           if constexpr (L::OPT) {
-            sW[ef * Np + m] = vp;                           // layer 0, ell_0 = 1
-            sW[(NPAIR + ef) * Np + m] = vu;
+            sW[ef * NPS + m] = vp;                           // layer 0, ell_0 = 1
+            sW[(NPAIR + ef) * NPS + m] = vu;
           } else {
-            T g[6];
-            load6(sgs + e * kGeoSurf + f * 6, g);
+            const int e = ef >> 2, f = ef & 3, fm = f * Nfp + m;
+            const T* gsf = sgs + e * kGeoSurf + f * 6;
             svq[e * 4 * Nfp + fm] = vp;
-            svq[(KE + e) * 4 * Nfp + fm] = g[0] * vu;
-            svq[(2 * KE + e) * 4 * Nfp + fm] = g[1] * vu;
-            svq[(3 * KE + e) * 4 * Nfp + fm] = g[2] * vu;
+            svq[(KE + e) * 4 * Nfp + fm] = gsf[0] * vu;
+            svq[(2 * KE + e) * 4 * Nfp + fm] = gsf[1] * vu;
+            svq[(3 * KE + e) * 4 * Nfp + fm] = gsf[2] * vu;
           }
         }
         if constexpr (L::OPT) {
@@ -516,50 +518,44 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
             constexpr int off_lo = layer_off(N, j), off_hi = layer_off(N, j - 1);
             constexpr int cofs = tet_dim(ml - 1);
             __syncwarp();
-            for (int it = lane; it < PPW * nlo; it += 32) {
-              const int pw = it / nlo, i = it - pw * nlo;
-              const int ef = warp * PPW + pw;
-              if (ef >= NPAIR) continue;
-              const ushort4 c = cpos[cofs + i];
-              const V4<T> cc = ccoef[cofs + i];
-              T* Wp = sW + ef * Np;
-              T* Wu = sW + (NPAIR + ef) * Np;
-              Wp[off_lo + i] = cc.x * Wp[off_hi + c.x] + cc.y * Wp[off_hi + c.y] + cc.z * Wp[off_hi + c.z];
-              Wu[off_lo + i] = cc.x * Wu[off_hi + c.x] + cc.y * Wu[off_hi + c.y] + cc.z * Wu[off_hi + c.z];
+            for (int i = lane; i < PPW * nlo; i += 32) {
+              const int pw = i / nlo, ii = i - pw * nlo;
+              const int ef = wg * PPW + pw;
+              const ushort4 c = cpos[cofs + ii];
+              const V4<T> cc = ccoef[cofs + ii];
+              T* Wp = sW + ef * NPS;
+              T* Wu = sW + (NPAIR + ef) * NPS;
+              Wp[off_lo + ii] = cc.x * Wp[off_hi + c.x] + cc.y * Wp[off_hi + c.y] + cc.z * Wp[off_hi + c.z];
+              Wu[off_lo + ii] = cc.x * Wu[off_hi + c.x] + cc.y * Wu[off_hi + c.y] + cc.z * Wu[off_hi + c.z];
             }
           });
         }
       } else {
         // dense lift input: the raw flux, velocity flux pre-scaled by the face normals
-        for (int it = lane; it < PPW * Nfp; it += 32) {
-          const int pw = it / Nfp, m = it - pw * Nfp;
-          const int ef = warp * PPW + pw;
-          if (ef >= NPAIR) continue;
+        for (int i = lane; i < PPW * Nfp; i += 32) {
+          const int pw = i / Nfp, m = i - pw * Nfp;
+          const int ef = wg * PPW + pw;
           const int e = ef >> 2, f = ef & 3, fm = f * Nfp + m;
-          T g[6];
-          load6(sgs + e * kGeoSurf + f * 6, g);
-          const T fu = sflux[(KE + e) * 4 * Nfp + fm];
-          svq[e * 4 * Nfp + fm] = sflux[e * 4 * Nfp + fm];
-          svq[(KE + e) * 4 * Nfp + fm] = g[0] * fu;
-          svq[(2 * KE + e) * 4 * Nfp + fm] = g[1] * fu;
-          svq[(3 * KE + e) * 4 * Nfp + fm] = g[2] * fu;
+          const T* gsf = sgs + e * kGeoSurf + f * 6;
+          const T fu = sflux[(NPAIR + ef) * NFS + m];
+          svq[e * 4 * Nfp + fm] = sflux[ef * NFS + m];
+          svq[(KE + e) * 4 * Nfp + fm] = gsf[0] * fu;
+          svq[(2 * KE + e) * 4 * Nfp + fm] = gsf[1] * fu;
+          svq[(3 * KE + e) * 4 * Nfp + fm] = gsf[2] * fu;
         }
       }
-      // V1 reuses the flux region; the epilogue reads every warp's faces
-      __syncthreads();
     }
 
     // ------------------------------------------------------------- volume V1 (BB, degree N-1)
     if constexpr (L::VOL && L::BB) {
-      for (int t = tid; t < KE * Npm; t += kThreads) {
+      for (int t = gtid; t < KE * Npm; t += GT) {
         const int e = t / Npm, b = t - e * Npm;
         const ushort4 c = v1chl[b];
-        T gv[12];
-        load12(sgv + e * kGeoVol, gv);
+        const T* gv = sgv + e * kGeoVol;
         T d[4][3];
 #pragma unroll
         for (int F = 0; F < 4; ++F) {
-          const T* qe = sq + (F * KE + e) * Np;
+          const T* qe = sq[F] + e * Np;
           const T q0 = qe[c.x], q1 = qe[c.y], q2 = qe[c.z], q3 = qe[c.w];
           // children b+e_0..b+e_3: Delta_m = q[b+e_{m+1}] - q[b+e_0]  (exactly 0 for constant states)
           d[F][0] = q1 - q0;
@@ -580,20 +576,24 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
         w[0] = sk * div;
       }
     }
-    __syncthreads();
+    group_sync<GT>(g);
 
     // ------------------------------------------------------------- V2 + surface gather + epilogue
+    uint32_t res_rest = 0;
+    const T* sres[4] = {nullptr, nullptr, nullptr, nullptr};
     if constexpr (L::RES) {
-      if (res_tma) mbar_wait(&bars[2], it & 1);
-    }
+      mbar_wait(&bars[2], it & 1);
+      res_rest = rest[2];
 #pragma unroll
-    for (int k = 0; k < EP_ITEMS; ++k) {
-      const int t = tid + k * kThreads;
-      if (t >= KE * Np) break;
+      for (int F = 0; F < 4; ++F)
+        sres[F] = reinterpret_cast<const T*>(gb + L::g_res + F * L::cq + win_off(p.res + F * fs + k0 * Np));
+    }
+    T* outF = p.out + k0 * Np;
+    T* resF = p.res + k0 * Np;
+    for (int t = gtid; t < KE * Np; t += GT) {
       const int e = t / Np, a = t - e * Np;
       const bool live = e < nv;
-      T gv[12];
-      load12(sgv + e * kGeoVol, gv);
+      const T* gv = sgv + e * kGeoVol;
       T r[4] = {T(0), T(0), T(0), T(0)};
       if constexpr (L::VOL) {
         if constexpr (L::BB) {
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
           }
         } else {
           // nodal NPT volume: dense Dr/Ds/Dt rows, coalesced transposed reads via L1
-          T gr[4] = {}, gs[4] = {}, gt[4] = {};
+          T gr[4] = {}, gsd[4] = {}, gt[4] = {};
           const T* d0 = p.dT;
           const T* d1 = p.dT + Np * Np;
           const T* d2 = p.dT + 2 * Np * Np;
@@ -615,19 +615,19 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
             const T x0 = ldg(d0 + b * Np + a), x1 = ldg(d1 + b * Np + a), x2 = ldg(d2 + b * Np + a);
 #pragma unroll
             for (int F = 0; F < 4; ++F) {
-              const T v = sq[(F * KE + e) * Np + b];
+              const T v = sq[F][e * Np + b];
               gr[F] += x0 * v;
-              gs[F] += x1 * v;
+              gsd[F] += x1 * v;
               gt[F] += x2 * v;
             }
           }
 #pragma unroll
           for (int i = 0; i < 3; ++i)
-            r[1 + i] = -gv[10] * (gv[0 * 3 + i] * gr[0] + gv[1 * 3 + i] * gs[0] + gv[2 * 3 + i] * gt[0]);
+            r[1 + i] = -gv[10] * (gv[0 * 3 + i] * gr[0] + gv[1 * 3 + i] * gsd[0] + gv[2 * 3 + i] * gt[0]);
           T div = T(0);
 #pragma unroll
           for (int i = 0; i < 3; ++i)
-            div += gv[0 * 3 + i] * gr[1 + i] + gv[1 * 3 + i] * gs[1 + i] + gv[2 * 3 + i] * gt[1 + i];
+            div += gv[0 * 3 + i] * gr[1 + i] + gv[1 * 3 + i] * gsd[1 + i] + gv[2 * 3 + i] * gt[1 + i];
           r[0] = -gv[9] * div;
         }
       }
@@ -635,18 +635,15 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
         T s[4] = {T(0), T(0), T(0), T(0)};
         if constexpr (L::OPT) {
           const ushort4 li = lidx[a];
-          const T* Wp = sW + e * 4 * Np;
-          const T* Wu = sW + (KE + e) * 4 * Np;
           const unsigned short lf[4] = {li.x, li.y, li.z, li.w};
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
-            T g[6];
-            load6(sgs + e * kGeoSurf + f * 6, g);
-            const T cu = Wu[f * Np + lf[f]];
-            s[0] += Wp[f * Np + lf[f]];
-            s[1] += g[0] * cu;
-            s[2] += g[1] * cu;
-            s[3] += g[2] * cu;
+            const T* gsf = sgs + e * kGeoSurf + f * 6;
+            const T cu = sW[(KE * 4 + e * 4 + f) * NPS + lf[f]];
+            s[0] += sW[(e * 4 + f) * NPS + lf[f]];
+            s[1] += gsf[0] * cu;
+            s[2] += gsf[1] * cu;
+            s[3] += gsf[2] * cu;
           }
         } else if constexpr (L::FAC) {
           const uint16_t* cols = p.el_cols + a * p.el_w;
@@ -677,9 +674,10 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
           // res = A res + dt rhs; q_out = q_in + B res   (reference solver.py:211-213)
 #pragma unroll
           for (int F = 0; F < 4; ++F) {
-            T x = (res_tma ? sres[F * KE * Np + t] : ldg(resF + F * fs + t)) * p.rk_a;
+            const T r0 = ((res_rest >> F) & 1) ? ldg(resF + F * fs + t) : sres[F][t];
+            T x = r0 * p.rk_a;
             x = x + p.dt * r[F];
-            const T qn = sq[F * KE * Np + t] + p.rk_b * x;
+            const T qn = sq[F][t] + p.rk_b * x;
             st_stream(resF + F * fs + t, x);
             st_stream(outF + F * fs + t, qn);
           }
@@ -693,7 +691,7 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(const Params<T> p) {
         }
       }
     }
-    __syncthreads();  // stage buffer + work buffers free for the next tile
+    group_sync<GT>(g);  // stage / res / work buffers free for the next tile
   }
 }
 

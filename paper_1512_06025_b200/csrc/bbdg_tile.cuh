@@ -92,6 +92,9 @@ template <int N> __host__ __device__ constexpr int group_warps() {
   constexpr int gw[10] = {0, 4, 4, 4, 4, 4, 4, 4, 4, 4};
   return gw[N];
 }
+#ifndef BBDG_MAX_CTA_THREADS
+#define BBDG_MAX_CTA_THREADS 1024
+#endif
 
 // ----------------------------------------------------------------------------
 // shared-memory layout
@@ -113,18 +116,25 @@ template <typename T, int N, int OP, int LIFT, int BASIS> struct Layout {
   static constexpr bool BB = BASIS == BASIS_BERNSTEIN;
   static constexpr bool OPT = SURF && BB && LIFT == LIFT_OPTIMAL;
   static constexpr bool FAC = SURF && BB && LIFT == LIFT_FACTORIZED;
-  // CTA-wide tables (closed forms, built once)
-  static constexpr int o_v2par = 0;                                    // ushort4 [Np]  parents in P_{N-1}
-  static constexpr int o_v2coef = align16(o_v2par + 8 * Np);           // V4<T>  [Np]  alpha_j
-  static constexpr int o_v1chl = align16(o_v2coef + 4 * sz * Np);      // ushort4 [Npm] children in P_N
-  static constexpr int o_trace = align16(o_v1chl + 8 * Npm);           // ushort [4][Nfp]
+  // CTA-wide tables (closed forms, built once).  Factorial-scaled variables make the
+  // one-degree elevation / reduction sums coefficient-free:
+  //   V1 stores w/beta!, V2 = alpha! * sum of 4 parents, cascade u_j = kappa_j * sum of
+  //   3 children with u = w * b!, gather multiplies by 1/beta_f(alpha)!.
+  static constexpr int o_v2par = 0;                                    // ushort4 [Np]  parents (Npm = zero slot)
+  static constexpr int o_v2fac = align16(o_v2par + 8 * Np);           // T [Np]        alpha!
+  static constexpr int o_v1chl = align16(o_v2fac + sz * Np);           // ushort4 [Npm] children in P_N
+  static constexpr int o_v1ifac = align16(o_v1chl + 8 * Npm);          // T [Npm]       1/beta!
+  static constexpr int o_trace = align16(o_v1ifac + sz * Npm);         // ushort [4][Nfp]
   static constexpr int o_ptab = align16(o_trace + 2 * 4 * Nfp);        // ushort [6][Nfp]
-  static constexpr int o_l0pos = align16(o_ptab + 2 * 6 * Nfp);        // ushort4 [2*Nfp]
-  static constexpr int o_l0val = align16(o_l0pos + 16 * Nfp);          // V4<T> [2*Nfp]
-  static constexpr int o_cpos = align16(o_l0val + 8 * sz * Nfp);       // ushort4 [Npm]
-  static constexpr int o_ccoef = align16(o_cpos + 8 * Npm);            // V4<T> [Npm]
-  static constexpr int o_lidx = align16(o_ccoef + 4 * sz * Npm);       // ushort4 [Np]
-  static constexpr int tables = align16(o_lidx + 8 * Np);
+  static constexpr int o_l0posA = align16(o_ptab + 2 * 6 * Nfp);       // ushort4 [Nfp]
+  static constexpr int o_l0posB = align16(o_l0posA + 8 * Nfp);         // ushort4 [Nfp]
+  static constexpr int o_l0valA = align16(o_l0posB + 8 * Nfp);         // V4<T> [Nfp]  (row scaled by b!)
+  static constexpr int o_l0valB = align16(o_l0valA + 4 * sz * Nfp);    // V4<T> [Nfp]
+  static constexpr int o_cb0 = align16(o_l0valB + 4 * sz * Nfp);       // uint8 [Npm]  row b0 of cascade item
+  static constexpr int o_lidx = align16(o_cb0 + Npm);                  // ushort4 [Np]
+  static constexpr int o_gfac = align16(o_lidx + 8 * Np);              // V4<T> [Np]   1/beta_f(alpha)!
+  static constexpr int o_fifac = align16(o_gfac + 4 * sz * Np);        // T [Nfp]      1/b! of face point
+  static constexpr int tables = align16(o_fifac + sz * Nfp);
   // per-group block.  Staged chunks get 32 B slack: TMA copies the 16-byte
   // aligned window around each chunk and the consumer offsets its pointer.
   static constexpr int cq = align16(KE * Np * sz) + 32;
@@ -146,12 +156,13 @@ template <typename T, int N, int OP, int LIFT, int BASIS> struct Layout {
   static constexpr int g_W = align16(g_vq + n_vq * sz);
   static constexpr int n_W = OPT ? 2 * KE * 4 * NPS : 0;
   static constexpr int g_w = align16(g_W + n_W * sz);
-  static constexpr int n_w = (VOL && BB) ? 4 * KE * Npm : 0;
+  static constexpr int NWS = Npm + 1;        // V1 row stride: slot Npm holds the V2 sentinel zero
+  static constexpr int n_w = (VOL && BB) ? 4 * KE * NWS : 0;
   static constexpr int g_bar = align16(g_w + n_w * sz);                // 3 mbarriers + 3 fallback masks
   static constexpr int group_bytes = align16(g_bar + 40);
   // groups per CTA: one CTA per SM with up to 1024 threads, so the tables exist once per SM
   static constexpr int ng_fit(int budget) {
-    for (int n = 1024 / GT; n >= 1; --n)
+    for (int n = BBDG_MAX_CTA_THREADS / GT; n >= 1; --n)
       if (tables + n * group_bytes <= budget) return n;
     return 0;
   }
@@ -178,41 +189,58 @@ __device__ __forceinline__ void decode2(int M, int i, int& b0, int& b1) {
   b1 = r;
 }
 
+__host__ __device__ constexpr double factorial(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= double(i);
+  return f;
+}
+// kappa_j = ell_j / (ell_{j-1} (N-j+1)): the factorial-scaled one-degree reduction factor
+__host__ __device__ constexpr double cascade_kappa(int N, int j) { return ell_of(N, j) / ell_of(N, j - 1) / double(N - j + 1); }
+
 template <typename T, int N, class L> __device__ void build_tables(unsigned char* sm, int tid, int nthreads) {
   constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm;
   ushort4* v2par = reinterpret_cast<ushort4*>(sm + L::o_v2par);
-  V4<T>* v2coef = reinterpret_cast<V4<T>*>(sm + L::o_v2coef);
+  T* v2fac = reinterpret_cast<T*>(sm + L::o_v2fac);
   ushort4* v1chl = reinterpret_cast<ushort4*>(sm + L::o_v1chl);
+  T* v1ifac = reinterpret_cast<T*>(sm + L::o_v1ifac);
   uint16_t* trace = reinterpret_cast<uint16_t*>(sm + L::o_trace);
   uint16_t* ptab = reinterpret_cast<uint16_t*>(sm + L::o_ptab);
-  ushort4* l0pos = reinterpret_cast<ushort4*>(sm + L::o_l0pos);
-  V4<T>* l0val = reinterpret_cast<V4<T>*>(sm + L::o_l0val);
-  ushort4* cpos = reinterpret_cast<ushort4*>(sm + L::o_cpos);
-  V4<T>* ccoef = reinterpret_cast<V4<T>*>(sm + L::o_ccoef);
+  ushort4* l0posA = reinterpret_cast<ushort4*>(sm + L::o_l0posA);
+  ushort4* l0posB = reinterpret_cast<ushort4*>(sm + L::o_l0posB);
+  V4<T>* l0valA = reinterpret_cast<V4<T>*>(sm + L::o_l0valA);
+  V4<T>* l0valB = reinterpret_cast<V4<T>*>(sm + L::o_l0valB);
+  uint8_t* cb0 = reinterpret_cast<uint8_t*>(sm + L::o_cb0);
   ushort4* lidx = reinterpret_cast<ushort4*>(sm + L::o_lidx);
+  V4<T>* gfac = reinterpret_cast<V4<T>*>(sm + L::o_gfac);
+  T* fifac = reinterpret_cast<T*>(sm + L::o_fifac);
   for (int i = tid; i < Np; i += nthreads) {
     int a0, a1, a2;
     decode3(N, i, a0, a1, a2);
     const int a[4] = {a0, a1, a2, N - a0 - a1 - a2};
-    // V2: alpha_j * w[alpha - e_j] (sentinel position 0, value 0, where alpha_j = 0)
-    v2par[i] = make_ushort4(a[0] ? pos3(N - 1, a0 - 1, a1, a2) : 0, a[1] ? pos3(N - 1, a0, a1 - 1, a2) : 0,
-                            a[2] ? pos3(N - 1, a0, a1, a2 - 1) : 0, a[3] ? pos3(N - 1, a0, a1, a2) : 0);
-    v2coef[i] = V4<T>{T(a[0]), T(a[1]), T(a[2]), T(a[3])};
-    // layer-major index of alpha in each face's cascade buffer
+    // V2: alpha! * sum_j what[alpha - e_j]; lanes with alpha_j = 0 read the zero slot Npm
+    v2par[i] = make_ushort4(a[0] ? pos3(N - 1, a0 - 1, a1, a2) : Npm, a[1] ? pos3(N - 1, a0, a1 - 1, a2) : Npm,
+                            a[2] ? pos3(N - 1, a0, a1, a2 - 1) : Npm, a[3] ? pos3(N - 1, a0, a1, a2) : Npm);
+    v2fac[i] = T(factorial(a[0]) * factorial(a[1]) * factorial(a[2]) * factorial(a[3]));
+    // layer-major index of alpha in each face's cascade buffer and 1/beta_f(alpha)!
     unsigned short li[4];
+    T gf[4];
     for (int f = 0; f < 4; ++f) {
-      int b[3], s = 0;
+      int bb[3], s = 0;
       for (int v = 0; v < 4; ++v)
-        if (v != f) b[s++] = a[v];
-      li[f] = layer_off(N, a[f]) + pos2(N - a[f], b[0], b[1]);
+        if (v != f) bb[s++] = a[v];
+      li[f] = layer_off(N, a[f]) + pos2(N - a[f], bb[0], bb[1]);
+      gf[f] = T(1.0 / (factorial(bb[0]) * factorial(bb[1]) * factorial(bb[2])));
     }
     lidx[i] = make_ushort4(li[0], li[1], li[2], li[3]);
+    gfac[i] = V4<T>{gf[0], gf[1], gf[2], gf[3]};
   }
   for (int i = tid; i < Npm; i += nthreads) {
     int b0, b1, b2;
     decode3(N - 1, i, b0, b1, b2);
+    const int b3 = N - 1 - b0 - b1 - b2;
     v1chl[i] = make_ushort4(pos3(N, b0 + 1, b1, b2), pos3(N, b0, b1 + 1, b2), pos3(N, b0, b1, b2 + 1),
                             pos3(N, b0, b1, b2));
+    v1ifac[i] = T(1.0 / (factorial(b0) * factorial(b1) * factorial(b2) * factorial(b3)));
   }
   for (int m = tid; m < Nfp; m += nthreads) {
     int b0, b1;
@@ -230,11 +258,13 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
       for (int k = 0; k < 3; ++k) nb[perms[s2][k]] = b[k];
       ptab[s2 * Nfp + m] = pos2(N, nb[0], nb[1]);
     }
-    // L0 row m: diag 1/2 sum (b_j+1)^2; (j,k) lane 1/2 (b_j+1) b_k at b + e_j - e_k
+    // L0 row m: diag 1/2 sum (b_j+1)^2; (j,k) lane 1/2 (b_j+1) b_k at b + e_j - e_k;
+    // the row is scaled by b! so its output is the factorial-scaled cascade level 0
+    const double bf = factorial(b[0]) * factorial(b[1]) * factorial(b[2]);
+    fifac[m] = T(1.0 / bf);
     unsigned short pp[8];
     T cv[8];
-    cv[0] = T(0.5 * double((b[0] + 1) * (b[0] + 1) + (b[1] + 1) * (b[1] + 1) + (b[2] + 1) * (b[2] + 1)));
-    pp[0] = m;
+    cv[0] = T(bf * 0.5 * double((b[0] + 1) * (b[0] + 1) + (b[1] + 1) * (b[1] + 1) + (b[2] + 1) * (b[2] + 1)));
     int l = 1;
     for (int j = 0; j < 3; ++j)
       for (int k = 0; k < 3; ++k) {
@@ -244,25 +274,21 @@ template <typename T, int N, class L> __device__ void build_tables(unsigned char
         gg[k] -= 1;
         const bool ok = b[k] >= 1;
         pp[l] = ok ? pos2(N, gg[0], gg[1]) : m;
-        cv[l] = ok ? T(0.5 * double((b[j] + 1) * b[k])) : T(0);
+        cv[l] = ok ? T(bf * 0.5 * double((b[j] + 1) * b[k])) : T(0);
         ++l;
       }
-    l0pos[2 * m] = make_ushort4(pp[1], pp[2], pp[3], pp[4]);
-    l0pos[2 * m + 1] = make_ushort4(pp[5], pp[6], 0, 0);
-    l0val[2 * m] = V4<T>{cv[0], cv[1], cv[2], cv[3]};
-    l0val[2 * m + 1] = V4<T>{cv[4], cv[5], cv[6], T(0)};
+    l0posA[m] = make_ushort4(pp[1], pp[2], pp[3], pp[4]);
+    l0posB[m] = make_ushort4(pp[5], pp[6], m, m);
+    l0valA[m] = V4<T>{cv[0], cv[1], cv[2], cv[3]};
+    l0valB[m] = V4<T>{cv[4], cv[5], cv[6], T(0)};
   }
-  // cascade item (target degree ml, point b): children b+e_k in degree ml+1, coefficients
-  // (b_k+1)/(ml+1) * ell_j/ell_{j-1} (j = N - ml): the buffer holds ell-scaled layers
+  // cascade item (target degree ml, index i): its row b0 (children at i+b0, i+b0+1, i+ml+2)
   for (int t = tid; t < Npm; t += nthreads) {
     int r = t, ml = 0;
     while (r >= tri_dim(ml)) { r -= tri_dim(ml); ++ml; }
     int b0, b1;
     decode2(ml, r, b0, b1);
-    const int b2 = ml - b0 - b1, j = N - ml;
-    cpos[t] = make_ushort4(pos2(ml + 1, b0 + 1, b1), pos2(ml + 1, b0, b1 + 1), pos2(ml + 1, b0, b1), 0);
-    const double ratio = ell_of(N, j) / ell_of(N, j - 1) / double(ml + 1);
-    ccoef[t] = V4<T>{T(double(b0 + 1) * ratio), T(double(b1 + 1) * ratio), T(double(b2 + 1) * ratio), T(0)};
+    cb0[t] = (uint8_t)b0;
   }
 }
 
@@ -354,15 +380,19 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
   extern __shared__ __align__(128) unsigned char sm[];
 
   const ushort4* v2par = reinterpret_cast<const ushort4*>(sm + L::o_v2par);
-  const V4<T>* v2coef = reinterpret_cast<const V4<T>*>(sm + L::o_v2coef);
+  const T* v2fac = reinterpret_cast<const T*>(sm + L::o_v2fac);
   const ushort4* v1chl = reinterpret_cast<const ushort4*>(sm + L::o_v1chl);
+  const T* v1ifac = reinterpret_cast<const T*>(sm + L::o_v1ifac);
   const uint16_t* trace = reinterpret_cast<const uint16_t*>(sm + L::o_trace);
   const uint16_t* ptab = reinterpret_cast<const uint16_t*>(sm + L::o_ptab);
-  const ushort4* l0pos = reinterpret_cast<const ushort4*>(sm + L::o_l0pos);
-  const V4<T>* l0val = reinterpret_cast<const V4<T>*>(sm + L::o_l0val);
-  const ushort4* cpos = reinterpret_cast<const ushort4*>(sm + L::o_cpos);
-  const V4<T>* ccoef = reinterpret_cast<const V4<T>*>(sm + L::o_ccoef);
+  const ushort4* l0posA = reinterpret_cast<const ushort4*>(sm + L::o_l0posA);
+  const ushort4* l0posB = reinterpret_cast<const ushort4*>(sm + L::o_l0posB);
+  const V4<T>* l0valA = reinterpret_cast<const V4<T>*>(sm + L::o_l0valA);
+  const V4<T>* l0valB = reinterpret_cast<const V4<T>*>(sm + L::o_l0valB);
+  const uint8_t* cb0 = reinterpret_cast<const uint8_t*>(sm + L::o_cb0);
   const ushort4* lidx = reinterpret_cast<const ushort4*>(sm + L::o_lidx);
+  const V4<T>* gfac = reinterpret_cast<const V4<T>*>(sm + L::o_gfac);
+  const T* fifac = reinterpret_cast<const T*>(sm + L::o_fifac);
 
   const int tid = threadIdx.x;
   const int g = tid / GT;            // group
@@ -374,7 +404,8 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
   T* sflux = reinterpret_cast<T*>(gb + L::g_flux);   // [grp][ef][NFS]
   T* svq = reinterpret_cast<T*>(gb + L::g_vq);       // [F][e][4 Nfp]
   T* sW = reinterpret_cast<T*>(gb + L::g_W);         // [grp][ef][NPS] layer-major, ell-scaled
-  T* sw = reinterpret_cast<T*>(gb + L::g_w);         // [F][e][Npm]
+  T* sw = reinterpret_cast<T*>(gb + L::g_w);         // [F][e][NWS], factorial-scaled, slot Npm = 0
+  constexpr int NWS = L::NWS;
 
   build_tables<T, N, L>(sm, tid, L::threads);
   if (gtid == 0) {
@@ -490,43 +521,48 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
           const int ef = wg * PPW + pw;
           const T* Fp = sflux + ef * NFS;
           const T* Fu = sflux + (NPAIR + ef) * NFS;
-          const ushort4 pa = l0pos[2 * m], pb = l0pos[2 * m + 1];
-          const V4<T> ca = l0val[2 * m], cb = l0val[2 * m + 1];
+          const ushort4 pa = l0posA[m], pb = l0posB[m];
+          const V4<T> ca = l0valA[m], cb = l0valB[m];
           const T vp = ca.x * Fp[m] + ca.y * Fp[pa.x] + ca.z * Fp[pa.y] + ca.w * Fp[pa.z] + cb.x * Fp[pa.w] +
                        cb.y * Fp[pb.x] + cb.z * Fp[pb.y];
           const T vu = ca.x * Fu[m] + ca.y * Fu[pa.x] + ca.z * Fu[pa.y] + ca.w * Fu[pa.z] + cb.x * Fu[pa.w] +
                        cb.y * Fu[pb.x] + cb.z * Fu[pb.y];
           if constexpr (L::OPT) {
-            sW[ef * NPS + m] = vp;                           // layer 0, ell_0 = 1
+            sW[ef * NPS + m] = vp;                           // layer 0 (ell_0 = 1), scaled by b!
             sW[(NPAIR + ef) * NPS + m] = vu;
           } else {
+            // the factorized mode takes the unscaled L0 output
             const int e = ef >> 2, f = ef & 3, fm = f * Nfp + m;
             const T* gsf = sgs + e * kGeoSurf + f * 6;
-            svq[e * 4 * Nfp + fm] = vp;
-            svq[(KE + e) * 4 * Nfp + fm] = gsf[0] * vu;
-            svq[(2 * KE + e) * 4 * Nfp + fm] = gsf[1] * vu;
-            svq[(3 * KE + e) * 4 * Nfp + fm] = gsf[2] * vu;
+            const T ib = fifac[m];
+            const T vpu = vp * ib, vuu = vu * ib;
+            svq[e * 4 * Nfp + fm] = vpu;
+            svq[(KE + e) * 4 * Nfp + fm] = gsf[0] * vuu;
+            svq[(2 * KE + e) * 4 * Nfp + fm] = gsf[1] * vuu;
+            svq[(3 * KE + e) * 4 * Nfp + fm] = gsf[2] * vuu;
           }
         }
         if constexpr (L::OPT) {
-          // S3 (optimal, Alg. 1): N one-degree reduction sweeps per face, both groups;
-          // layer j = (E^{N-j+1}_{N-j})^T layer j-1, stored ell_j-scaled
+          // S3 (optimal, Alg. 1): N one-degree reduction sweeps per face, both groups, in
+          // factorial-scaled form: u_j[b] = kappa_j (u_{j-1}[b+e0] + u_{j-1}[b+e1] + u_{j-1}[b+e2])
           static_for<1, N + 1>([&](auto J) {
             constexpr int j = decltype(J)::value;
             constexpr int ml = N - j;
             constexpr int nlo = tri_dim(ml);
             constexpr int off_lo = layer_off(N, j), off_hi = layer_off(N, j - 1);
             constexpr int cofs = tet_dim(ml - 1);
+            const T kap = T(cascade_kappa(N, j));
             __syncwarp();
             for (int i = lane; i < PPW * nlo; i += 32) {
               const int pw = i / nlo, ii = i - pw * nlo;
               const int ef = wg * PPW + pw;
-              const ushort4 c = cpos[cofs + ii];
-              const V4<T> cc = ccoef[cofs + ii];
-              T* Wp = sW + ef * NPS;
-              T* Wu = sW + (NPAIR + ef) * NPS;
-              Wp[off_lo + ii] = cc.x * Wp[off_hi + c.x] + cc.y * Wp[off_hi + c.y] + cc.z * Wp[off_hi + c.z];
-              Wu[off_lo + ii] = cc.x * Wu[off_hi + c.x] + cc.y * Wu[off_hi + c.y] + cc.z * Wu[off_hi + c.z];
+              const int b0 = cb0[cofs + ii];
+              const T* sp = sW + ef * NPS + off_hi + ii;
+              const T* su = sW + (NPAIR + ef) * NPS + off_hi + ii;
+              const T up = (sp[b0] + sp[b0 + 1]) + sp[ml + 2];
+              const T uu = (su[b0] + su[b0 + 1]) + su[ml + 2];
+              sW[ef * NPS + off_lo + ii] = kap * up;
+              sW[(NPAIR + ef) * NPS + off_lo + ii] = kap * uu;
             }
           });
         }
@@ -548,6 +584,7 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
 
     // ------------------------------------------------------------- volume V1 (BB, degree N-1)
     if constexpr (L::VOL && L::BB) {
+      if (gtid < 4 * KE) sw[gtid * NWS + Npm] = T(0);   // V2 sentinel slots
       for (int t = gtid; t < KE * Npm; t += GT) {
         const int e = t / Npm, b = t - e * Npm;
         const ushort4 c = v1chl[b];
@@ -563,12 +600,13 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
           d[F][2] = q3 - q0;
         }
         const T half = T(0.5);
-        const T sr = -half * gv[10];   // -(1/rho)/2
-        const T sk = -half * gv[9];    // -kappa/2
-        T* w = sw + e * Npm + b;
+        const T ib = v1ifac[b];
+        const T sr = -half * gv[10] * ib;   // -(1/rho)/2 / beta!
+        const T sk = -half * gv[9] * ib;    // -kappa/2 / beta!
+        T* w = sw + e * NWS + b;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
-          w[(1 + i) * KE * Npm] = sr * (gv[0 * 3 + i] * d[0][0] + gv[1 * 3 + i] * d[0][1] + gv[2 * 3 + i] * d[0][2]);
+          w[(1 + i) * KE * NWS] = sr * (gv[0 * 3 + i] * d[0][0] + gv[1 * 3 + i] * d[0][1] + gv[2 * 3 + i] * d[0][2]);
         T div = T(0);
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -598,11 +636,11 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
       if constexpr (L::VOL) {
         if constexpr (L::BB) {
           const ushort4 pp = v2par[a];
-          const V4<T> al = v2coef[a];
+          const T af = v2fac[a];
 #pragma unroll
           for (int F = 0; F < 4; ++F) {
-            const T* w = sw + (F * KE + e) * Npm;
-            r[F] = al.x * w[pp.x] + al.y * w[pp.y] + al.z * w[pp.z] + al.w * w[pp.w];
+            const T* w = sw + (F * KE + e) * NWS;
+            r[F] = af * ((w[pp.x] + w[pp.y]) + (w[pp.z] + w[pp.w]));
           }
         } else {
           // nodal NPT volume: dense Dr/Ds/Dt rows, coalesced transposed reads via L1
@@ -635,12 +673,14 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
         T s[4] = {T(0), T(0), T(0), T(0)};
         if constexpr (L::OPT) {
           const ushort4 li = lidx[a];
+          const V4<T> gf4 = gfac[a];
           const unsigned short lf[4] = {li.x, li.y, li.z, li.w};
+          const T gf[4] = {gf4.x, gf4.y, gf4.z, gf4.w};
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
             const T* gsf = sgs + e * kGeoSurf + f * 6;
-            const T cu = sW[(KE * 4 + e * 4 + f) * NPS + lf[f]];
-            s[0] += sW[(e * 4 + f) * NPS + lf[f]];
+            const T cu = gf[f] * sW[(KE * 4 + e * 4 + f) * NPS + lf[f]];
+            s[0] += gf[f] * sW[(e * 4 + f) * NPS + lf[f]];
             s[1] += gsf[0] * cu;
             s[2] += gsf[1] * cu;
             s[3] += gsf[2] * cu;

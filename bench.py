@@ -159,18 +159,32 @@ def run_ours(args, rank, world):
     from paper_1512_06025_b200 import cube_mesh, lsrk4_step, FieldState, stable_dt
     from paper_1512_06025_b200.solver import RK4A, RK4B
 
-    dev = rank % max(1, torch.cuda.device_count())
+    dev = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     dtype = np.float32 if args.dtype == "f32" else np.float64
     s = 4 if args.dtype == "f32" else 8
-    mesh = cube_mesh(args.n)
-    K = mesh.K
+    if world > 1:
+        # weak scaling: a box of world x n^3 cells, one n^3-cell x-slab per rank
+        from paper_1512_06025_b200.mesh import box_mesh
+
+        mesh = box_mesh(world * args.n, args.n, args.n, lo=(-0.5 * world, -0.5, -0.5), hi=(0.5 * world, 0.5, 0.5))
+    else:
+        mesh = cube_mesh(args.n)
+    K = mesh.K // world
     orders = parse_orders(args.orders)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     gen = torch.Generator(device="cuda").manual_seed(2024 + rank)
     systems = {}
     for N in orders:
-        sy = build_system(mesh, N, dtype)
+        if world > 1:
+            from paper_1512_06025_b200 import BernsteinRefOps, Materials
+            from paper_1512_06025_b200.dist import DistWaveSystem
+
+            sy = DistWaveSystem(mesh, BernsteinRefOps.build(N), Materials.homogeneous(mesh.K), dtype, rank, world,
+                                align=6 * args.n * args.n)
+            sy.Np, sy.torch_dtype = sy.local.Np, sy.local.torch_dtype
+        else:
+            sy = build_system(mesh, N, dtype)
         q = torch.randn((4, K, sy.Np), generator=gen, device="cuda", dtype=sy.torch_dtype)
         systems[N] = dict(sy=sy, q=q, q2=torch.empty_like(q), res=torch.randn_like(q), rhs=torch.empty_like(q),
                           dt=stable_dt(mesh, N, 1.0))
@@ -221,7 +235,7 @@ def run_ours(args, rank, world):
         ach = bytes_ / (t_stage * 1e-3) / 1e9
         row = {"gdofs_stage": 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
                "stage_gbs": ach, "stage_frac": ach / peak}
-        if not args.quick:
+        if not args.quick and world == 1:
             sy, q, rhs = d["sy"], d["q"], d["rhs"]
             reps = max(3, args.steps)
             tv = time_launches(torch, lambda: sy.volume_into(q, rhs), flush, reps)
@@ -262,7 +276,7 @@ def run_ours(args, rank, world):
     # end-to-end through the public API with host (numpy) buffers
     e2e_ms, h2d, d2h = 0.0, 0, 0
     e2e_reps = 2 if args.quick else max(2, min(args.steps, 5))
-    for N in orders:
+    for N in (orders if world == 1 else []):
         d = systems[N]
         host = torch.empty((4, K, d["sy"].Np), dtype=d["sy"].torch_dtype, pin_memory=True)
         host.copy_(d["q"])
@@ -278,7 +292,8 @@ def run_ours(args, rank, world):
         h2d += hq.nbytes
         d2h += hq.nbytes
     e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders) * e2e_reps
-    out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+    out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9 if e2e_ms else None, "unit": UNIT,
+                  "h2d_bytes_per_step": h2d,
                   "d2h_bytes_per_step": d2h,
                   "what": "lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"}
     return out, K
@@ -332,10 +347,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     orders = parse_orders(args.orders)
     dtype = np.float32 if args.dtype == "f32" else np.float64
-    config = {"workload": f"BB-DG acoustic LSRK4 stage sweep N={args.orders}, cube_mesh({args.n}) K={6 * args.n ** 3}, "
+    config = {"workload": f"BB-DG acoustic LSRK4 stage sweep N={args.orders}, cube_mesh({args.n}) K={6 * args.n ** 3}"
+                          f"{' per GPU (box of ' + str(world) + ' slabs)' if world > 1 else ''}, "
                           f"{args.lift} lift", "K": 6 * args.n ** 3, "orders": orders, "lift": args.lift,
               "l2": "flushed (256 MB write) before every timed launch", "materials": "homogeneous",
-              "parallelism": f"element-replica x{world}" if world > 1 else "1 GPU"}
+              "parallelism": f"element slabs x{world}, NCCL face-trace halo" if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:

@@ -82,6 +82,13 @@ int bbdg_rhs(bbdg_ctx* ctx, const void* q, void* rhs, int lift_mode, void* strea
 int bbdg_lsrk_stage(bbdg_ctx* ctx, const void* q_in, void* q_out, void* res, int lift_mode, double rk_a,
                     double rk_b, double dt, void* stream);
 
+/* Element-range variants for partitioned runs: only elements [k0, k1) are
+ * updated (neighbour traces are still read from the whole plane / halo), so
+ * interior elements can run while the face-trace halo is in flight. */
+int bbdg_lsrk_stage_range(bbdg_ctx* ctx, const void* q_in, void* q_out, void* res, int lift_mode, double rk_a,
+                          double rk_b, double dt, int64_t k0, int64_t k1, void* stream);
+int bbdg_rhs_range(bbdg_ctx* ctx, const void* q, void* rhs, int lift_mode, int64_t k0, int64_t k1, void* stream);
+
 /* The stand-alone LSRK update (solver.py:211-213) over n values, in place:
  *   res = rk_a*res + dt*rhs;  q += rk_b*res. */
 int bbdg_lsrk_update(int dtype, int64_t n, void* q, void* res, const void* rhs, double rk_a, double rk_b,

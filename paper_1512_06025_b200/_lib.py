@@ -36,6 +36,8 @@ SIGNATURES = [
     ("bbdg_surface", C.c_int, [_P, _P, _P, C.c_int, C.c_int, _P]),
     ("bbdg_rhs", C.c_int, [_P, _P, _P, C.c_int, _P]),
     ("bbdg_lsrk_stage", C.c_int, [_P, _P, _P, _P, C.c_int, _D, _D, _D, _P]),
+    ("bbdg_lsrk_stage_range", C.c_int, [_P, _P, _P, _P, C.c_int, _D, _D, _D, _I64, _I64, _P]),
+    ("bbdg_rhs_range", C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _P]),
     ("bbdg_lsrk_update", C.c_int, [C.c_int, _I64, _P, _P, _P, _D, _D, _D, _P]),
     ("bbdg_step", C.c_int, [_P, _P, _P, _P, _D, C.c_int, _P]),
     ("bbdg_halo_pack", C.c_int, [_P, _P, _P, _P, _I64, _P]),

@@ -208,6 +208,8 @@ static int num_sms_of_current_device() {
 template <typename T> static Params<T> make_params(const bbdg_ctx* c) {
   Params<T> p{};
   p.K = c->K;
+  p.kbeg = 0;
+  p.kend = c->K;
   p.geo_vol = static_cast<const T*>(c->geo_vol);
   p.geo_surf = static_cast<const T*>(c->geo_surf);
   p.nbr = c->nbr;
@@ -389,7 +391,13 @@ int bbdg_surface(bbdg_ctx* c, const void* q, void* rhs, int lift, int accumulate
 }
 
 int bbdg_rhs(bbdg_ctx* c, const void* q, void* rhs, int lift, void* stream) {
+  if (!c) return set_error(BBDG_ERR_ARG, "null context");
+  return bbdg_rhs_range(c, q, rhs, lift, 0, c->K, stream);
+}
+
+int bbdg_rhs_range(bbdg_ctx* c, const void* q, void* rhs, int lift, int64_t k0, int64_t k1, void* stream) {
   if (int rc = check_ctx(c)) return rc;
+  if (k0 < 0 || k1 > c->K || k0 > k1) return set_error(BBDG_ERR_ARG, "element range outside [0, K]");
   if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
   if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q");
   if (int rc = check_lift(c, lift, true)) return rc;
@@ -397,13 +405,22 @@ int bbdg_rhs(bbdg_ctx* c, const void* q, void* rhs, int lift, void* stream) {
     Params<T> p = make_params<T>(c);
     p.q = static_cast<const T*>(q);
     p.out = static_cast<T*>(rhs);
+    p.kbeg = k0;
+    p.kend = k1;
     return run<T>(c, OP_RHS, lift, p, stream);
   });
 }
 
 int bbdg_lsrk_stage(bbdg_ctx* c, const void* q_in, void* q_out, void* res, int lift, double rk_a, double rk_b,
                     double dt, void* stream) {
+  if (!c) return set_error(BBDG_ERR_ARG, "null context");
+  return bbdg_lsrk_stage_range(c, q_in, q_out, res, lift, rk_a, rk_b, dt, 0, c->K, stream);
+}
+
+int bbdg_lsrk_stage_range(bbdg_ctx* c, const void* q_in, void* q_out, void* res, int lift, double rk_a, double rk_b,
+                          double dt, int64_t k0, int64_t k1, void* stream) {
   if (int rc = check_ctx(c)) return rc;
+  if (k0 < 0 || k1 > c->K || k0 > k1) return set_error(BBDG_ERR_ARG, "element range outside [0, K]");
   if (!q_in || !q_out || !res) return set_error(BBDG_ERR_ARG, "null state pointer");
   if (q_in == q_out) return set_error(BBDG_ERR_ARG, "q_out must not alias q_in");
   if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
@@ -416,6 +433,8 @@ int bbdg_lsrk_stage(bbdg_ctx* c, const void* q_in, void* q_out, void* res, int l
     p.rk_a = T(rk_a);
     p.rk_b = T(rk_b);
     p.dt = T(dt);
+    p.kbeg = k0;
+    p.kend = k1;
     return run<T>(c, OP_STAGE, lift, p, stream);
   });
 }

@@ -29,7 +29,7 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
     blocks_per_sm = b;
   }
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
-  const int64_t ntiles = (p.K + L::KE - 1) / L::KE;
+  const int64_t ntiles = (p.kend - p.kbeg + L::KE - 1) / L::KE;
   if (ntiles == 0) return BBDG_OK;
   const int64_t grid = std::min<int64_t>((ntiles + L::NG - 1) / L::NG, (int64_t)num_sms * blocks_per_sm);
   kern<<<(unsigned)grid, L::threads, L::total, stream>>>(p);

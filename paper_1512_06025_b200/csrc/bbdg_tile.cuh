@@ -36,7 +36,8 @@ constexpr int kGeoVol = 12;   // rst_dx[m][i] (9), kappa, inv_rho, pad
 constexpr int kGeoSurf = 24;  // per face: n0 n1 n2 face_scale tau_p tau_u
 
 template <typename T> struct Params {
-  int64_t K;
+  int64_t K;             // elements in the state planes (plane stride K*Np)
+  int64_t kbeg, kend;    // element range this launch updates
   const T* q;            // (4,K,Np) stage input
   T* out;                // rhs, or q_out for OP_STAGE
   T* res;                // (4,K,Np) LSRK register (OP_STAGE)
@@ -416,14 +417,14 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
   }
   __syncthreads();
 
-  const int64_t ntiles = (p.K + KE - 1) / KE;
+  const int64_t ntiles = (p.kend - p.kbeg + KE - 1) / KE;
   const int64_t fs = p.K * Np;
   const int64_t stride = (int64_t)gridDim.x * NG;
   int64_t tile = (int64_t)blockIdx.x * NG + g;
   Chunk ch[8];
   if (gtid == 0 && tile < ntiles) {
-    const int64_t k0 = tile * KE;
-    const int nv = (int)(p.K - k0 < KE ? p.K - k0 : KE);
+    const int64_t k0 = p.kbeg + tile * KE;
+    const int nv = (int)(p.kend - k0 < KE ? p.kend - k0 : KE);
     const int n = tile_chunks<T, L>(p, k0, nv, 0, ch);
     rest[0] = issue_chunks(ch, n, gb, &bars[0]);
   }
@@ -432,16 +433,16 @@ __global__ void __launch_bounds__(Layout<T, N, OP, LIFT, BASIS>::threads, 1) til
   for (int it = 0; tile < ntiles; tile += stride, ++it) {
     const int st = it & 1;
     unsigned char* stage = gb + st * L::stage_bytes;
-    const int64_t k0 = tile * KE;
-    const int nv = (int)(p.K - k0 < KE ? p.K - k0 : KE);
+    const int64_t k0 = p.kbeg + tile * KE;
+    const int nv = (int)(p.kend - k0 < KE ? p.kend - k0 : KE);
     // producer: next tile into the other stage buffer (freed by the last group barrier),
     // this tile's LSRK register into the res buffer (consumed by the epilogue)
     const int64_t nt = tile + stride;
     if (gtid == 0) {
       fence_proxy_async();
       if (nt < ntiles) {
-        const int64_t k1 = nt * KE;
-        const int nv1 = (int)(p.K - k1 < KE ? p.K - k1 : KE);
+        const int64_t k1 = p.kbeg + nt * KE;
+        const int nv1 = (int)(p.kend - k1 < KE ? p.kend - k1 : KE);
         const int n = tile_chunks<T, L>(p, k1, nv1, (st ^ 1) * L::stage_bytes, ch);
         rest[st ^ 1] = issue_chunks(ch, n, gb, &bars[st ^ 1]);
       }

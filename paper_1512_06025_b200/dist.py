@@ -1,0 +1,63 @@
+"""Element-partitioned BB-DG across ranks (one GPU per rank) with a face-trace halo.
+
+Each rank owns a contiguous element slab (``partition.slab_ranges``) and a
+``WaveSystem`` over it whose cut faces read a halo buffer.  One LSRK stage:
+
+    pack own traces of cut faces        (bbdg_halo_pack, current stream)
+    post grouped NCCL send/recv         (torch.distributed.batch_isend_irecv)
+    stage the interior element range    (overlaps the exchange)
+    wait for the halo
+    stage the halo-dependent end ranges (bbdg_lsrk_stage_range)
+
+No other collective is involved; results are bitwise equal to the single-GPU
+stage because the per-element arithmetic does not change (tested).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .partition import HaloExchanger, build_halo_plan, slab_ranges
+from .solver import RK4A, RK4B, WaveSystem
+
+
+class DistWaveSystem:
+    def __init__(self, mesh, ops, materials, dtype=np.float64, rank=0, world=1, dist=None, align=1):
+        import torch
+
+        ranges = slab_ranges(mesh.K, world, align)
+        self.plan = build_halo_plan(mesh, world, rank, ranges)
+        self.local = WaveSystem(mesh, ops, materials, dtype, _plan=self.plan)
+        self.torch = torch
+        self.ex = HaloExchanger(self.plan, self.local.ops.Nfp, self.local.torch_dtype, "cuda",
+                                self.local.halo_pack, dist)
+        self.local.set_halo(self.ex.recv, self.plan.nhalo)
+        self.interior, self.halo_ranges = self.plan.launch_ranges()
+
+    @property
+    def K(self):
+        return self.plan.n_local
+
+    def empty_state(self):
+        return self.local.empty_state()
+
+    def post(self, q_in):
+        return self.ex.post(q_in)
+
+    def stage_into(self, q_in, q_out, res, a, b, dt, lift_mode="optimal", reqs=None):
+        """One fused LSRK stage of this rank's slab; `reqs` lets a caller pre-post the exchange."""
+        if reqs is None:
+            reqs = self.post(q_in)
+        if self.interior is not None:
+            self.local.stage_range_into(q_in, q_out, res, a, b, dt, lift_mode, *self.interior)
+        self.ex.wait(reqs)
+        for k0, k1 in self.halo_ranges:
+            self.local.stage_range_into(q_in, q_out, res, a, b, dt, lift_mode, k0, k1)
+
+    def step_into(self, q, q_tmp, res, dt, lift_mode="optimal"):
+        """lsrk4_step on the slab: five exchanged stages, result left in q."""
+        res.zero_()
+        bufs = [q, q_tmp]
+        for s in range(5):
+            self.stage_into(bufs[s & 1], bufs[(s + 1) & 1], res, RK4A[s], RK4B[s], dt, lift_mode)
+        q.copy_(q_tmp)

@@ -90,10 +90,11 @@ class FieldState:
 class WaveSystem:
     """Mesh + operators + materials bound to a device context (solver.py:96-193)."""
 
-    def __init__(self, mesh: Mesh, ops, materials: Materials, dtype=np.float64):
+    def __init__(self, mesh: Mesh, ops, materials: Materials, dtype=np.float64, _plan=None):
         if len(materials.kappa) != mesh.K:
             raise ValueError("materials sized for a different mesh")
         self.mesh = mesh
+        self._plan = _plan          # partition.HaloPlan for an element-partitioned rank
         self.ops_double = ops
         self.dtype = np.dtype(dtype).type
         if self.dtype not in (np.float32, np.float64):
@@ -115,6 +116,12 @@ class WaveSystem:
         self.kappa = materials.kappa.astype(self.dtype)[:, None]
         self.inv_kappa = (1.0 / materials.kappa).astype(self.dtype)[:, None]
         self.inv_rho = (1.0 / materials.rho).astype(self.dtype)[:, None]
+        if _plan is not None:
+            sl = slice(_plan.k0, _plan.k1)
+            for name in ("tau_p", "tau_u", "face_scale", "normals", "rst_dx", "kappa", "inv_kappa", "inv_rho"):
+                setattr(self, name, getattr(self, name)[sl])
+            self._tau_p64, self._tau_u64, self._fscale64 = (self._tau_p64[sl], self._tau_u64[sl],
+                                                            self._fscale64[sl])
         self._gather = None
         self._torch = _torch()
         self._lib = _lib.load()
@@ -126,10 +133,15 @@ class WaveSystem:
         L = self._lib
         ctx = C.c_void_p()
         _lib.check(L.bbdg_ctx_create(self.ops.N, _lib.BASIS[self.basis], _lib.DTYPE[np.dtype(self.dtype).name],
-                                     mesh.K, C.byref(ctx)), "bbdg_ctx_create")
-        nbr, code = mesh.face_codes()
+                                     self.K, C.byref(ctx)), "bbdg_ctx_create")
+        if self._plan is None:
+            sl = slice(0, mesh.K)
+            nbr, code = mesh.face_codes()
+        else:
+            sl = slice(self._plan.k0, self._plan.k1)
+            nbr, code = self._plan.nbr, self._plan.code
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
-                (mesh.rst_dx, materials.kappa, 1.0 / materials.rho, mesh.normals,
+                (mesh.rst_dx[sl], materials.kappa[sl], 1.0 / materials.rho[sl], mesh.normals[sl],
                  self._fscale64, self._tau_p64, self._tau_u64)]
         nbr = np.ascontiguousarray(nbr, dtype=np.int32)
         code = np.ascontiguousarray(code, dtype=np.int8)
@@ -160,7 +172,8 @@ class WaveSystem:
 
     @property
     def K(self) -> int:
-        return self.mesh.K
+        """Elements this system updates (the rank's slab for a partitioned system)."""
+        return self.mesh.K if self._plan is None else self._plan.n_local
 
     @property
     def Np(self) -> int:
@@ -233,6 +246,22 @@ class WaveSystem:
         _lib.check(self._lib.bbdg_lsrk_stage(self._ctx, q_in.data_ptr(), q_out.data_ptr(), res.data_ptr(),
                                              self._lift_id(lift_mode), float(a), float(b), float(dt),
                                              self._stream()), "bbdg_lsrk_stage")
+
+    def stage_range_into(self, q_in, q_out, res, a, b, dt, lift_mode, k0, k1):
+        _lib.check(self._lib.bbdg_lsrk_stage_range(self._ctx, q_in.data_ptr(), q_out.data_ptr(), res.data_ptr(),
+                                                   self._lift_id(lift_mode), float(a), float(b), float(dt),
+                                                   int(k0), int(k1), self._stream()), "bbdg_lsrk_stage_range")
+
+    def halo_pack(self, q, faces, out):
+        """bbdg_halo_pack: traces of (elem, face) pairs -> out (4, n, Nfp)."""
+        if faces.shape[0] == 0:
+            return
+        _lib.check(self._lib.bbdg_halo_pack(self._ctx, q.data_ptr(), out.data_ptr(), faces.data_ptr(),
+                                            int(faces.shape[0]), self._stream()), "bbdg_halo_pack")
+
+    def set_halo(self, halo, nhalo):
+        _lib.check(self._lib.bbdg_ctx_set_halo(self._ctx, halo.data_ptr() if nhalo else None, int(nhalo)),
+                   "bbdg_ctx_set_halo")
 
     def step_into(self, q, q_tmp, res, dt, lift_mode="factorized"):
         _lib.check(self._lib.bbdg_step(self._ctx, q.data_ptr(), q_tmp.data_ptr(), res.data_ptr(), float(dt),

@@ -1,0 +1,197 @@
+"""Element partition + face-trace halo: host logic on CPU (plans, a real
+2-process gloo exchange) and bitwise partition invariance of the kernels on one GPU."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1512_06025_b200 import mesh as msh
+from paper_1512_06025_b200.bernstein import BernsteinRefOps
+from paper_1512_06025_b200.multiindex import face_permutation_table
+from paper_1512_06025_b200.partition import HaloExchanger, build_halo_plan, pack_traces_reference, slab_ranges
+
+
+def expected_neighbour_reads(m, q, N, k, f):
+    """What the single-domain kernel reads for face (k, f): the neighbour's trace,
+    permuted into k's face-point order (reference gather, mesh.py:158-188)."""
+    ops = BernsteinRefOps.build(N)
+    g, _ = msh.build_trace_maps(m, ops.trace, ops.Np)
+    return q.reshape(4, -1)[:, g[k, f]]
+
+
+def halo_reads(plan, recv, N, k_loc, f):
+    """What the partitioned kernel reads: recv[:, slot, ptab[perm][m]]."""
+    code = int(plan.code[k_loc, f]) & 0xFF
+    s = (code >> 2) & 7
+    slot = int(plan.nbr[k_loc, f])
+    return recv[:, slot, face_permutation_table(N)[s]]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_plan_roundtrip_matches_single_domain_gather(P):
+    m = msh.cube_mesh(3)
+    N = 3
+    ops = BernsteinRefOps.build(N)
+    q = np.random.default_rng(1).standard_normal((4, m.K, ops.Np))
+    ranges = slab_ranges(m.K, P, align=6 * 9)
+    plans = [build_halo_plan(m, P, r, ranges) for r in range(P)]
+    # every face is owned exactly once; local neighbour ids stay inside the slab
+    assert sum(p.n_local for p in plans) == m.K
+    for p in plans:
+        loc = ((p.code.astype(np.int32) >> 6) & 1) == 0
+        assert np.all((p.nbr[loc] >= 0) & (p.nbr[loc] < p.n_local))
+    # simulated exchange with the host packer
+    for p in plans:
+        recv = np.zeros((4, max(p.nhalo, 1), ops.Nfp))
+        for s, cnt in p.recv_count.items():
+            sender = plans[s]
+            faces = sender.send[p.rank]
+            assert len(faces) == cnt
+            qs = q[:, sender.k0:sender.k1]
+            recv[:, p.recv_offset[s]:p.recv_offset[s] + cnt] = pack_traces_reference(qs, faces, ops.trace)
+        kk, ff = np.nonzero(((p.code.astype(np.int32) >> 6) & 1) == 1)
+        assert len(kk) == p.nhalo
+        for k_loc, f in zip(kk, ff):
+            got = halo_reads(p, recv, N, k_loc, f)
+            want = expected_neighbour_reads(m, q, N, p.k0 + k_loc, f)
+            assert np.array_equal(got, want)
+
+
+def test_launch_ranges_cover_slab():
+    m = msh.cube_mesh(12)                      # 3 x-slabs of cells per rank
+    ranges = slab_ranges(m.K, 4, align=6 * 144)
+    for r in range(4):
+        p = build_halo_plan(m, 4, r, ranges)
+        inner, outer = p.launch_ranges()
+        cover = np.zeros(p.n_local, dtype=int)
+        for a, b in ([inner] if inner else []) + outer:
+            cover[a:b] += 1
+        assert np.all(cover == 1)
+        if inner:
+            assert not np.isin(np.arange(*inner), p.halo_elems).any()
+            assert inner[1] - inner[0] >= p.n_local // 4    # the middle slab overlaps the exchange
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = msh.cube_mesh(3)
+        N = 2
+        ops = BernsteinRefOps.build(N)
+        q = np.random.default_rng(7).standard_normal((4, m.K, ops.Np))
+        plan = build_halo_plan(m, world, rank)
+        trace = torch.as_tensor(ops.trace)
+
+        def packer(qt, faces, outb):
+            outb.copy_(qt[:, faces[:, 0].long()[:, None], trace[faces[:, 1].long()]])
+
+        ex = HaloExchanger(plan, ops.Nfp, torch.float64, "cpu", packer)
+        ql = torch.as_tensor(q[:, plan.k0:plan.k1].copy())
+        ex.wait(ex.post(ql))
+        recv = ex.recv.numpy()
+        kk, ff = np.nonzero(((plan.code.astype(np.int32) >> 6) & 1) == 1)
+        ok = all(np.array_equal(halo_reads(plan, recv, N, k, f),
+                                expected_neighbour_reads(m, q, N, plan.k0 + k, f)) for k, f in zip(kk, ff))
+        out[rank] = int(ok and len(kk) > 0)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_rank_halo_exchange():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert dict(out) == {0: 1, 1: 1}
+
+
+# ---------------------------------------------------------------------------- GPU
+class _FakeWorld:
+    """In-process communicator: P ranks on one GPU exchange by device copies."""
+
+    def __init__(self):
+        self.sends, self.recvs = {}, {}
+
+    def flush(self):
+        for key, rs in self.recvs.items():
+            for s, r in zip(self.sends.get(key, []), rs):
+                r.copy_(s)
+        self.sends, self.recvs = {}, {}
+
+
+class _FakeDist:
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def P2POp(op, t, peer):
+        return (op, t, peer)
+
+    def isend(self, *a):
+        raise AssertionError("not called directly")
+
+    def irecv(self, *a):
+        raise AssertionError("not called directly")
+
+    def batch_isend_irecv(self, ops):
+        for op, t, peer in ops:
+            if op == self.isend:
+                self.world.sends.setdefault((self.rank, peer), []).append(t)
+            else:
+                self.world.recvs.setdefault((peer, self.rank), []).append(t)
+        world = self.world
+
+        class _Req:
+            def wait(self):
+                world.flush()
+
+        return [_Req()]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("dname", ["f64", "f32"])
+def test_partitioned_step_bitwise_equals_single_domain(P, dname):
+    import torch
+
+    from paper_1512_06025_b200 import Materials, WaveSystem, stable_dt
+    from paper_1512_06025_b200.dist import DistWaveSystem
+    from paper_1512_06025_b200.solver import RK4A, RK4B
+
+    dtype = np.float64 if dname == "f64" else np.float32
+    m = msh.cube_mesh(6)
+    N = 4
+    ops = BernsteinRefOps.build(N)
+    mat = Materials.homogeneous(m.K)
+    single = WaveSystem(m, ops, mat, dtype)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn((4, m.K, single.Np), dtype=single.torch_dtype, device="cuda", generator=g)
+    res0 = torch.randn_like(q)
+    dt = stable_dt(m, N, 1.0)
+    q_ref, res_ref = torch.empty_like(q), res0.clone()
+    single.stage_into(q, q_ref, res_ref, RK4A[2], RK4B[2], dt, "optimal")
+
+    world = _FakeWorld()
+    parts = [DistWaveSystem(m, ops, mat, dtype, r, P, dist=_FakeDist(world, r), align=6 * 36) for r in range(P)]
+    qs = [q[:, p.plan.k0:p.plan.k1].contiguous() for p in parts]
+    rs = [res0[:, p.plan.k0:p.plan.k1].contiguous() for p in parts]
+    outs = [torch.empty_like(x) for x in qs]
+    reqs = [p.post(x) for p, x in zip(parts, qs)]
+    for p, x, o, r, rq in zip(parts, qs, outs, rs, reqs):
+        p.stage_into(x, o, r, RK4A[2], RK4B[2], dt, "optimal", reqs=rq)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, dim=1), q_ref)
+    assert torch.equal(torch.cat(rs, dim=1), res_ref)

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libbbdg_cuda.so"
+LIB_PATH = Path(os.environ.get("BBDG_LIB") or Path(__file__).resolve().parent / "libbbdg_cuda.so")
 
 BASIS = {"bernstein": 0, "nodal": 1}
 DTYPE = {"float32": 0, "float64": 1}

@@ -55,6 +55,34 @@ def _units():
     return units
 
 
+def build_variant(out_dir: Path, defines: list[str], dtypes=("f32",), jobs: int | None = None) -> Path:
+    """Tuning build: the whole library with extra -D flags into out_dir (loaded via BBDG_LIB)."""
+    out_dir = Path(out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    exe = nvcc()
+    units = [u for u in _units() if u[0] == "bbdg_capi" or u[0].split("_")[1] in dtypes]
+    missing = [u for u in _units() if u not in units]
+
+    def compile_unit(u):
+        name, src, defs = u
+        obj = out_dir / f"{name}.o"
+        cmd = [exe, *ARCH, *FLAGS, *defs, *defines, "-c", str(src), "-o", str(obj)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {name}:\n{r.stderr}")
+        return obj
+
+    with ThreadPoolExecutor(jobs or os.cpu_count() or 1) as ex:
+        objs = list(ex.map(compile_unit, units))
+    objs += [BUILD / f"{u[0]}.o" for u in missing]   # untouched dtype units from the main build
+    lib = out_dir / "libbbdg_cuda.so"
+    r = subprocess.run([exe, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart"], capture_output=True,
+                       text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return lib
+
+
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> Path:
     digest = _sources_digest()
     stamp = BUILD / "digest"

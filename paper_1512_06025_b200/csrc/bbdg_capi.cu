@@ -7,7 +7,7 @@
 
 #include "bbdg_common.cuh"
 #include "bbdg_internal.h"
-#include "bbdg_tile.cuh"
+#include "bbdg_opt.cuh"
 
 struct bbdg_ctx {
   int N, basis, dtype;
@@ -16,6 +16,7 @@ struct bbdg_ctx {
   int num_sms;
   void* geo_vol = nullptr;   // T (K,12)
   void* geo_surf = nullptr;  // T (K,24)
+  void* geo = nullptr;       // T (K,36) fused record of the optimal-lift kernels (kGeoRec)
   int32_t* nbr = nullptr;    // (K,4)
   int32_t* code = nullptr;   // (K)
   void* el_vals = nullptr;   // T (Np,w)
@@ -82,12 +83,16 @@ static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa
                           const double* normals, const double* face_scale, const double* tau_p,
                           const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code) {
   const int64_t K = c->K;
-  std::vector<T> gv((size_t)K * kGeoVol, T(0)), gs((size_t)K * kGeoSurf);
+  std::vector<T> gv((size_t)K * kGeoVol, T(0)), gs((size_t)K * kGeoSurf), gr((size_t)K * kGeoRec, T(0));
   std::vector<int32_t> nb((size_t)K * 4), cd((size_t)K);
   for (int64_t k = 0; k < K; ++k) {
     for (int j = 0; j < 9; ++j) gv[k * kGeoVol + j] = static_cast<T>(rst_dx[k * 9 + j]);
     gv[k * kGeoVol + 9] = static_cast<T>(kappa[k]);
     gv[k * kGeoVol + 10] = static_cast<T>(inv_rho[k]);
+    T* r = &gr[k * kGeoRec];
+    r[24] = static_cast<T>(kappa[k]);
+    r[25] = static_cast<T>(inv_rho[k]);
+    for (int j = 0; j < 9; ++j) r[26 + j] = static_cast<T>(rst_dx[k * 9 + j]);
     uint32_t packed = 0;
     for (int f = 0; f < 4; ++f) {
       T* g = &gs[k * kGeoSurf + f * 6];
@@ -98,6 +103,12 @@ static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa
       const int32_t n = nbr_elem[k * 4 + f];
       const int code = static_cast<uint8_t>(nbr_code[k * 4 + f]);
       const bool halo = (code >> 6) & 1, bnd = (code >> 5) & 1;
+      // fused record: the boundary mirror (jp = -2 p-, solver.py:173) rides on the sign of Bs
+      const double hs = 0.5 * face_scale[k * 4 + f];
+      for (int i = 0; i < 3; ++i) r[4 * f + i] = static_cast<T>(normals[(k * 4 + f) * 3 + i]);
+      r[4 * f + 3] = static_cast<T>(bnd ? -hs : hs);
+      r[16 + 2 * f] = static_cast<T>(tau_p[k * 4 + f]);
+      r[17 + 2 * f] = static_cast<T>(hs * tau_u[k * 4 + f]);
       if (!bnd && !halo && (n < 0 || n >= K)) return set_error(BBDG_ERR_ARG, "neighbour element out of range");
       nb[k * 4 + f] = n;
       packed |= static_cast<uint32_t>(code) << (8 * f);
@@ -109,6 +120,8 @@ static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa
   cudaFree(c->geo_surf);
   cudaFree(c->nbr);
   cudaFree(c->code);
+  cudaFree(c->geo);
+  c->geo = upload(gr, &rc);
   c->geo_vol = upload(gv, &rc);
   c->geo_surf = upload(gs, &rc);
   c->nbr = static_cast<int32_t*>(upload(nb, &rc));
@@ -212,6 +225,7 @@ template <typename T> static Params<T> make_params(const bbdg_ctx* c) {
   p.kend = c->K;
   p.geo_vol = static_cast<const T*>(c->geo_vol);
   p.geo_surf = static_cast<const T*>(c->geo_surf);
+  p.geo = static_cast<const T*>(c->geo);
   p.nbr = c->nbr;
   p.code = c->code;
   p.halo = static_cast<const T*>(c->halo);
@@ -286,6 +300,7 @@ void bbdg_ctx_destroy(bbdg_ctx* c) {
   if (!c) return;
   cudaFree(c->geo_vol);
   cudaFree(c->geo_surf);
+  cudaFree(c->geo);
   cudaFree(c->nbr);
   cudaFree(c->code);
   cudaFree(c->el_vals);

@@ -2,7 +2,7 @@
 // dtype combinations build in parallel.  Exposes a launcher table entry
 // through a C++ symbol named after the pair.
 #include "bbdg_internal.h"
-#include "bbdg_tile.cuh"
+#include "bbdg_opt.cuh"
 
 #ifndef BBDG_T
 #error "BBDG_T (float|double) must be defined"
@@ -14,30 +14,66 @@
 namespace bbdg {
 namespace {
 
-template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t stream, int num_sms) {
+// persistent launch: grid = min(#groups needed, SMs x resident CTAs), one CTA
+// holds NG independent element groups
+template <class KernT, int THREADS, int TOTAL, int KE, int NG>
+int launch_persistent(KernT kern, int& blocks_per_sm, const void* vp, cudaStream_t stream, int num_sms) {
   using T = BBDG_T;
-  using L = Layout<T, BBDG_N, OP, LIFT, BASIS>;
-  static int blocks_per_sm = -1;
-  auto kern = tile_kernel<T, BBDG_N, OP, LIFT, BASIS>;
   if (blocks_per_sm < 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TOTAL);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, L::threads, L::total);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, THREADS, TOTAL);
     if (e != cudaSuccess) return set_cuda_error(e, "occupancy");
     if (b < 1) return set_error(BBDG_ERR_UNSUPPORTED, "tile kernel does not fit on an SM");
     blocks_per_sm = b;
   }
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
-  const int64_t ntiles = (p.kend - p.kbeg + L::KE - 1) / L::KE;
+  const int64_t ntiles = (p.kend - p.kbeg + KE - 1) / KE;
   if (ntiles == 0) return BBDG_OK;
-  const int64_t grid = std::min<int64_t>((ntiles + L::NG - 1) / L::NG, (int64_t)num_sms * blocks_per_sm);
-  kern<<<(unsigned)grid, L::threads, L::total, stream>>>(p);
+  const int64_t grid = std::min<int64_t>((ntiles + NG - 1) / NG, (int64_t)num_sms * blocks_per_sm);
+  kern<<<(unsigned)grid, THREADS, TOTAL, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "tile kernel launch");
 }
 
-template <int OP, int LIFT, int BASIS> int64_t smem() { return Layout<BBDG_T, BBDG_N, OP, LIFT, BASIS>::total; }
+template <int OP, int FSR> int launch_opt(const void* vp, cudaStream_t stream, int num_sms) {
+  using T = BBDG_T;
+  using L = OptLayout<T, BBDG_N, OP, FSR>;
+  static int blocks_per_sm = -1;
+  return launch_persistent<decltype(&opt_kernel<T, BBDG_N, OP, FSR>), L::threads, L::total, L::KE, L::NG>(
+      opt_kernel<T, BBDG_N, OP, FSR>, blocks_per_sm, vp, stream, num_sms);
+}
+
+template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t stream, int num_sms) {
+  using T = BBDG_T;
+  if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) {
+    // field-plane stride residue (K Np) mod (16 / sizeof(T)) selects the smem field stride
+    const Params<T>& p = *static_cast<const Params<T>*>(vp);
+    constexpr int A = 16 / sizeof(T);
+    const int fsr = (int)((p.K * Dims<BBDG_N>::Np) % A);
+    if constexpr (A == 4) {
+      switch (fsr) {
+        case 0: return launch_opt<OP, 0>(vp, stream, num_sms);
+        case 1: return launch_opt<OP, 1>(vp, stream, num_sms);
+        case 2: return launch_opt<OP, 2>(vp, stream, num_sms);
+        default: return launch_opt<OP, 3>(vp, stream, num_sms);
+      }
+    } else {
+      return fsr ? launch_opt<OP, 1>(vp, stream, num_sms) : launch_opt<OP, 0>(vp, stream, num_sms);
+    }
+  } else {
+    static int blocks_per_sm = -1;
+    using L = Layout<T, BBDG_N, OP, LIFT, BASIS>;
+    return launch_persistent<decltype(&tile_kernel<T, BBDG_N, OP, LIFT, BASIS>), L::threads, L::total, L::KE, L::NG>(
+        tile_kernel<T, BBDG_N, OP, LIFT, BASIS>, blocks_per_sm, vp, stream, num_sms);
+  }
+}
+
+template <int OP, int LIFT, int BASIS> int64_t smem() {
+  if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) return OptLayout<BBDG_T, BBDG_N, OP, 0>::total;
+  else return Layout<BBDG_T, BBDG_N, OP, LIFT, BASIS>::total;
+}
 
 }  // namespace
 
@@ -45,7 +81,7 @@ template <int OP, int LIFT, int BASIS> int64_t smem() { return Layout<BBDG_T, BB
 #define BBDG_CAT(a, b, c) BBDG_CAT_(a, b, c)
 
 KernelEntry BBDG_CAT(entry, BBDG_TNAME, BBDG_N)(int op, int lift, int basis) {
-  KernelEntry k{nullptr, nullptr, group_elems<BBDG_N>()};
+  KernelEntry k{nullptr, nullptr, OptLayout<BBDG_T, BBDG_N, OP_STAGE, 0>::KE};
 #define BBDG_CASE(O, Lf, B)                            \
   if (op == O && lift == Lf && basis == B) {           \
     k.launch = &launch<O, Lf, B>;                      \

@@ -1,0 +1,676 @@
+// Bernstein-Bezier fused kernels for the optimal lift (reference lift_mode
+// "optimal", bernstein.py:313-329) -- the bench's hot path.
+//
+// Same per-tile algorithm as tile_kernel (bbdg_tile.cuh: S1 flux, S2 L0,
+// S3 one-degree reduction cascade, V1/V2 factored volume, fused LSRK
+// epilogue), laid out so that the instruction stream is almost only
+// shared-memory loads and FMAs:
+//
+//  * TMA bulk staging (cp.async.bulk + mbarrier) of the next tile's state
+//    planes, LSRK register and geometry.  A bulk copy moves a 16-byte aligned
+//    window, so each field lands at its own sub-16-byte shift; the smem field
+//    stride S is chosen congruent to the global plane stride K*Np modulo
+//    16/sizeof(T) (template parameter FSR), which makes every field's shift
+//    equal to field 0's.  All four fields (and res) of a tile then sit at
+//    compile-time distances from one per-tile base: a stencil load is one LDS
+//    with an immediate offset.
+//  * Per-thread work is fixed across tiles (a persistent group always
+//    processes KE-element tiles), so every stencil offset / table index of a
+//    thread's items is computed once in the prologue and kept in registers
+//    (u16 pairs) for the whole launch.  Slots that are full for every thread
+//    are unguarded at compile time (no divergence bookkeeping).
+//  * The neighbour face traces of the next tile are gathered with cp.async
+//    into shared memory while the current tile computes (connectivity words
+//    are loaded a phase earlier); one smem table maps (neighbour face,
+//    orientation, point) to the neighbour's trace position.
+//  * One 36-word geometry record per element (kGeoRec) replaces the 12 +
+//    24-word volume / surface records; the boundary mirror condition
+//    (jp = -2 p, solver.py:173) is folded into the sign of the face scale.
+//
+// Phases per group tile (reference solver.py:139-214):
+//   S1  upwind flux at every face point (warp-local faces)   solver.py:166-184
+//   S2  L0 on (Fp, Fu), <=7 closed-form lanes                bernstein.py:221-229
+//   S3  N reduction sweeps (Alg. 1), factorial-scaled         bernstein.py:313-329
+//   V1  Delta_m (degree N-1) contracted with rst_dx           solver.py:139-158
+//   --- group barrier
+//   V2  one-degree elevation; gather of the 4 lifted faces; epilogue
+//       (rhs store/accumulate, or res = A res + dt rhs; q_out = q + B res)
+//   --- group barrier
+#pragma once
+#include "bbdg_tile.cuh"
+
+namespace bbdg {
+
+// Per-element geometry record (dtype T), built by bbdg_ctx_set_geometry:
+//   [4f+0..2] outward normal of face f      [4f+3] Bs_f = +-face_scale_f / 2 (negative on boundary faces)
+//   [16+2f]   tau_p of face f               [17+2f] C_f = tau_u face_scale_f / 2
+//   [24] kappa   [25] 1/rho   [26+3m+i] rst_dx[m][i]   [35] 0
+// With jp = sgn(Bs) p+ - p- (p+ = own trace on boundary faces):
+//   Fp = tau_p |Bs| jp - |Bs| jun,  Fu = C jun - |Bs| jp
+// i.e. solver.py:175-181 (Fp = (tau_p jp - jun) fs/2, Fu = (tau_u jun - jp) fs/2).
+constexpr int kGeoRec = 36;
+
+template <typename T> struct alignas(2 * sizeof(T)) P2 {
+  T x, y;
+};
+
+// ----------------------------------------------------------------------------
+// cp.async (LDGSTS) helpers
+// ----------------------------------------------------------------------------
+template <int B> __device__ __forceinline__ void cp_async(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ----------------------------------------------------------------------------
+// configuration: elements per group tile; groups per CTA (4 warps per group)
+// ----------------------------------------------------------------------------
+// (tuning builds may override the tables: -DBBDG_OPT_KE4=0,32,... etc.)
+#ifndef BBDG_OPT_KE4
+#define BBDG_OPT_KE4 0, 32, 24, 12, 6, 4, 3, 2, 2, 1
+#endif
+#ifndef BBDG_OPT_KE8
+#define BBDG_OPT_KE8 0, 16, 12, 6, 4, 2, 2, 1, 1, 1
+#endif
+#ifndef BBDG_OPT_NG4
+#define BBDG_OPT_NG4 0, 4, 4, 4, 4, 4, 4, 4, 3, 4
+#endif
+#ifndef BBDG_OPT_NG8
+#define BBDG_OPT_NG8 0, 4, 4, 4, 4, 4, 4, 4, 4, 4
+#endif
+template <int N, int SZ> __host__ __device__ constexpr int opt_ke() {
+  constexpr int k4[10] = {BBDG_OPT_KE4};
+  constexpr int k8[10] = {BBDG_OPT_KE8};
+  return SZ == 4 ? k4[N] : k8[N];
+}
+template <int N, int SZ> __host__ __device__ constexpr int opt_max_groups() {
+  constexpr int g4[10] = {BBDG_OPT_NG4};
+  constexpr int g8[10] = {BBDG_OPT_NG8};
+  return SZ == 4 ? g4[N] : g8[N];
+}
+
+template <typename T, int N, int OP, int FSR> struct OptLayout {
+  using D = Dims<N>;
+  static constexpr int Np = D::Np, Nfp = D::Nfp, Npm = D::Npm;
+  static constexpr int sz = (int)sizeof(T);
+  static constexpr int A = 16 / sz;          // elements per 16 bytes
+  static_assert(FSR >= 0 && FSR < A, "FSR = (K Np) mod (16 / sizeof(T))");
+  static constexpr int KE = opt_ke<N, sz>();
+  static constexpr int GW = 4, GT = 32 * GW;
+  static constexpr bool VOL = OP != OP_SURFACE, SURF = OP != OP_VOLUME, RES = OP == OP_STAGE;
+  static constexpr int PPW = 4 * KE / GW;   // faces per warp
+  static_assert((4 * KE) % GW == 0, "faces must split evenly over the warps");
+  static constexpr int NFS = odd_up(Nfp), NPS = odd_up(Np), NWS = Npm + 1;
+  static constexpr int NQ = KE * Np;        // values per field per tile
+  static constexpr int NB = 4 * KE * NFS;   // face-point slots per field (nb / flux buffers)
+  // slot counts (items per thread, rounded up); a slot is "full" if every thread has an item
+  static constexpr int NS_ITEMS = PPW * Nfp;
+  static constexpr int SS = SURF ? (NS_ITEMS + 31) / 32 : 0;
+  static constexpr bool HOIST_L0 = SS <= 2;   // L0 lane offsets in registers (else one LDS.128 per item)
+  static constexpr int SV1 = VOL ? (KE * Npm + GT - 1) / GT : 0;
+  static constexpr int SV2 = (KE * Np + GT - 1) / GT;
+  // cascade items are single-field: 2 PPW face-fields x tri_dim(N-j) per warp at level j
+  static constexpr int s3_items(int j) { return 2 * PPW * tri_dim(N - j); }
+  static constexpr int s3_slots(int j) { return (s3_items(j) + 31) / 32; }
+  static constexpr int s3_base(int j) {
+    int o = 0;
+    for (int jj = 1; jj < j; ++jj) o += s3_slots(jj);
+    return o;
+  }
+  static constexpr int S3T = SURF ? s3_base(N + 1) : 0;
+  static constexpr int cas_u(int j) {   // largest u = 2 pw (ml+2) + 2 b0 of a cascade item at level j
+    return 2 * (PPW - 1) * (N - j + 2) + 2 * (N - j);
+  }
+  static_assert(cas_u(1) < 256, "8-bit cascade item offsets");
+  // CTA tables (bytes)
+  static constexpr int o_tr2 = 0;                                      // u16 [4 f2][6 perm][Nfp] neighbour trace pos
+  static constexpr int o_ptab = align16(o_tr2 + 2 * 24 * Nfp);         // u16 [6][Nfp] (halo faces)
+  static constexpr int o_l0c = align16(o_ptab + 2 * 6 * Nfp);          // V4<T> [2][Nfp]
+  static constexpr int o_gfac = align16(o_l0c + 2 * 4 * sz * Nfp);     // V4<T> [Np]
+  static constexpr int o_l0p = align16(o_gfac + 4 * sz * Np);          // u16 [Nfp][8] L0 lane positions
+  static constexpr int tables = align16(o_l0p + 16 * Nfp);
+  // stage (units of T; every block 16-byte aligned).  Field stride S = FSR (mod A).
+  static constexpr int rnd(int n) { return (n + A - 1) / A * A; }
+  static constexpr int S = rnd(NQ + 2 * A) + FSR;
+  static constexpr int t_q = 0;                                   // [4][S] + shift slack
+  static constexpr int t_res = rnd(t_q + 4 * S + 2 * A);          // same shape (RES)
+  static constexpr int t_geo = rnd(t_res + (RES ? 4 * S + 2 * A : 0));   // [KE][36]
+  static constexpr int t_nb = rnd(t_geo + KE * kGeoRec);          // [4][NB]
+  static constexpr int t_bar = rnd(t_nb + (SURF ? 4 * NB : 0));   // mbarrier (8 bytes)
+  static constexpr int stage_T = rnd(t_bar + 8 / sz + 1);
+  static constexpr int RQ = t_res - t_q;                          // res distance from q (elements)
+  // group block (units of T)
+  static constexpr int g_flux = 2 * stage_T;                      // [2][NB]
+  static constexpr int g_W = rnd(g_flux + (SURF ? 2 * NB : 0));   // [layer j][4KE face][tri(N-j)][p,u]
+  static constexpr int g_w = rnd(g_W + (SURF ? 8 * KE * Np : 0));   // [4][KE][NWS]
+  static constexpr int group_T = rnd(g_w + (VOL ? 4 * KE * NWS : 0));
+  static constexpr int group_bytes = group_T * sz;
+  static constexpr int ng_fit(int budget) {
+    for (int n = opt_max_groups<N, sz>(); n >= 1; --n)
+      if (tables + n * group_bytes <= budget) return n;
+    return 0;
+  }
+  static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
+  static constexpr int threads = NG * GT;
+  static constexpr int total = tables + NG * group_bytes;
+  static_assert(4 * KE * NPS < 65536 && KE * Np < 65536, "u16 offsets");
+};
+
+// L0 lane positions of face point m (lane order (j,k), j != k); missing lanes -> m
+template <int N> __device__ __forceinline__ void l0_lanes(int m, int pp[6]) {
+  int b0, b1;
+  decode2(N, m, b0, b1);
+  const int b[3] = {b0, b1, N - b0 - b1};
+  int l = 0;
+  for (int j = 0; j < 3; ++j)
+    for (int k = 0; k < 3; ++k) {
+      if (j == k) continue;
+      int g[3] = {b[0], b[1], b[2]};
+      g[j] += 1;
+      g[k] -= 1;
+      pp[l++] = b[k] >= 1 ? pos2(N, g[0], g[1]) : m;
+    }
+}
+
+template <typename T, int N, class L> __device__ void build_opt_tables(unsigned char* sm, int tid, int nthreads) {
+  constexpr int Np = L::Np, Nfp = L::Nfp;
+  uint16_t* tr2 = reinterpret_cast<uint16_t*>(sm + L::o_tr2);
+  uint16_t* ptab = reinterpret_cast<uint16_t*>(sm + L::o_ptab);
+  V4<T>* l0c = reinterpret_cast<V4<T>*>(sm + L::o_l0c);
+  V4<T>* gfac = reinterpret_cast<V4<T>*>(sm + L::o_gfac);
+  for (int i = tid; i < Np; i += nthreads) {
+    int a0, a1, a2;
+    decode3(N, i, a0, a1, a2);
+    const int a[4] = {a0, a1, a2, N - a0 - a1 - a2};
+    T gf[4];
+    for (int f = 0; f < 4; ++f) {
+      double d = 1.0;
+      for (int v = 0; v < 4; ++v)
+        if (v != f) d *= factorial(a[v]);
+      gf[f] = T(1.0 / d);
+    }
+    gfac[i] = V4<T>{gf[0], gf[1], gf[2], gf[3]};
+  }
+  for (int m = tid; m < Nfp; m += nthreads) {
+    int b0, b1;
+    decode2(N, m, b0, b1);
+    const int b[3] = {b0, b1, N - b0 - b1};
+    // PERMS3 order (multiindex.py): neighbour slot sig[k] holds local vertex k
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int s2 = 0; s2 < 6; ++s2) {
+      int nb[3];
+      for (int k = 0; k < 3; ++k) nb[perms[s2][k]] = b[k];
+      const int m2 = pos2(N, nb[0], nb[1]);
+      ptab[s2 * Nfp + m] = m2;
+      const int c[3] = {nb[0], nb[1], N - nb[0] - nb[1]};
+      for (int f2 = 0; f2 < 4; ++f2) {
+        int a[4], s = 0;
+        for (int v = 0; v < 4; ++v) a[v] = (v == f2) ? 0 : c[s++];
+        tr2[(f2 * 6 + s2) * Nfp + m] = pos3(N, a[0], a[1], a[2]);
+      }
+    }
+    // L0 row m scaled by b!: diag 1/2 sum (b_j+1)^2, lane (j,k) 1/2 (b_j+1) b_k (bernstein.py:221-229)
+    const double bf = factorial(b[0]) * factorial(b[1]) * factorial(b[2]);
+    T cv[8];
+    cv[0] = T(bf * 0.5 * double((b[0] + 1) * (b[0] + 1) + (b[1] + 1) * (b[1] + 1) + (b[2] + 1) * (b[2] + 1)));
+    int l = 1;
+    for (int j = 0; j < 3; ++j)
+      for (int k = 0; k < 3; ++k) {
+        if (j == k) continue;
+        cv[l++] = b[k] >= 1 ? T(bf * 0.5 * double((b[j] + 1) * b[k])) : T(0);
+      }
+    cv[7] = T(0);
+    int pp[6];
+    l0_lanes<N>(m, pp);
+    uint16_t* l0p = reinterpret_cast<uint16_t*>(sm + L::o_l0p) + 8 * m;
+    for (int x = 0; x < 6; ++x) l0p[x] = pp[x];
+    l0p[6] = l0p[7] = 0;
+    l0c[m] = V4<T>{cv[0], cv[1], cv[2], cv[3]};
+    l0c[Nfp + m] = V4<T>{cv[4], cv[5], cv[6], cv[7]};
+  }
+}
+
+__device__ __forceinline__ uint32_t lo16(uint32_t x) { return x & 0xffffu; }
+__device__ __forceinline__ uint32_t hi16(uint32_t x) { return x >> 16; }
+__device__ __forceinline__ uint32_t pk(uint32_t a, uint32_t b) { return a | (b << 16); }
+
+// run f() for slot K of a phase with `count` items spread over `width` threads;
+// full slots are unguarded at compile time
+template <int K, int WIDTH, int COUNT, class F> __device__ __forceinline__ void slot(int idx, F&& f) {
+  if constexpr ((K + 1) * WIDTH <= COUNT) {
+    f();
+  } else if constexpr (K * WIDTH < COUNT) {
+    if (idx + K * WIDTH < COUNT) f();
+  }
+}
+
+template <typename T, int N, int OP, int FSR>
+__global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kernel(const Params<T> p) {
+  using L = OptLayout<T, N, OP, FSR>;
+  constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm, KE = L::KE, NG = L::NG, GT = L::GT, A = L::A;
+  constexpr int NPS = L::NPS, NFS = L::NFS, NWS = L::NWS, NB = L::NB, PPW = L::PPW, S = L::S;
+  constexpr int SS = L::SS, SV1 = L::SV1, SV2 = L::SV2, NSI = L::NS_ITEMS;
+  constexpr int sz = (int)sizeof(T);
+  extern __shared__ __align__(128) unsigned char sm[];
+
+  const uint16_t* tr2 = reinterpret_cast<const uint16_t*>(sm + L::o_tr2);
+  const uint16_t* ptab = reinterpret_cast<const uint16_t*>(sm + L::o_ptab);
+  const V4<T>* l0c = reinterpret_cast<const V4<T>*>(sm + L::o_l0c);
+  const V4<T>* gfac = reinterpret_cast<const V4<T>*>(sm + L::o_gfac);
+
+  const int tid = threadIdx.x;
+  const int g = tid / GT;
+  const int gtid = tid - g * GT;
+  // logical warp role, rotated per group: warp w of every group sits on SMSP w, so rotating
+  // the roles gives each scheduler one warp of every role (the roles' work differs)
+  const int lane = tid & 31, wg = ((gtid >> 5) + g) % L::GW;
+  const int ltid = wg * 32 + lane;   // logical thread index within the group
+  T* gbase = reinterpret_cast<T*>(sm + L::tables + g * L::group_bytes);
+  P2<T>* sflux = reinterpret_cast<P2<T>*>(gbase + L::g_flux);   // [4KE][NFS] (Fp, Fu)
+  T* sW = gbase + L::g_W;   // [layer j][4KE face][tri(N-j)][p,u], ell- and factorial-scaled
+  T* sw = gbase + L::g_w;         // [4][KE][NWS], slot Npm = 0
+  auto stage_ptr = [&](int st) { return gbase + st * L::stage_T; };
+  auto stage_bar = [&](int st) { return reinterpret_cast<uint64_t*>(stage_ptr(st) + L::t_bar); };
+
+  build_opt_tables<T, N, L>(sm, tid, L::threads);
+  if constexpr (L::VOL) {
+    for (int i = gtid; i < 4 * KE; i += GT) sw[i * NWS + Npm] = T(0);   // V2 sentinel slots (never rewritten)
+  }
+  if (ltid == 0) {
+    mbar_init(stage_bar(0), 1);
+    mbar_init(stage_bar(1), 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------------- prologue: hoisted per-thread offsets
+  constexpr int SSa = SS > 0 ? SS : 1;
+  uint32_t s_of[SSa];   // own-trace offset | face-point slot (flux / nb buffers)
+  uint32_t s_ef[SSa];   // m | f << 8 | e << 10  (bits 8.. = face index ef = 4e + f)
+  uint32_t s_l0[L::HOIST_L0 ? SSa : 1][3];   // six L0 lane offsets in the flux buffer
+#pragma unroll
+  for (int k = 0; k < SS; ++k) {
+    const int i = lane + 32 * k;
+    const bool ok = i < NSI;
+    const int pw = ok ? i / Nfp : 0, m = ok ? i - pw * Nfp : 0;
+    const int ef = wg * PPW + pw, e = ef >> 2, f = ef & 3;
+    s_of[k] = pk(e * Np + tr2[(f * 6) * Nfp + m], ef * NFS + m);
+    s_ef[k] = m | (f << 8) | (e << 10);
+    if constexpr (L::HOIST_L0) {
+      int pp[6];
+      l0_lanes<N>(m, pp);
+      s_l0[k][0] = pk(ef * NFS + pp[0], ef * NFS + pp[1]);
+      s_l0[k][1] = pk(ef * NFS + pp[2], ef * NFS + pp[3]);
+      s_l0[k][2] = pk(ef * NFS + pp[4], ef * NFS + pp[5]);
+    }
+  }
+  // cascade items (level j, single field), 16 bits each, two per register: u | v << 8 with
+  // u = 2 pw (ml+2) + 2 b0, v = 2 b0 (tri(ml+1) - tri(ml) = ml+2).  Item i of the warp writes W at Bw_j + i and reads its
+  // children at Br_j + i + u + {0, 2} and Br_j + i + u - v + 2 (ml+2)   (see S3 below)
+  uint32_t c3[(L::S3T + 1) / 2 > 0 ? (L::S3T + 1) / 2 : 1];
+  if constexpr (L::SURF) {
+#pragma unroll
+    for (int x = 0; x < (L::S3T + 1) / 2; ++x) c3[x] = 0;
+    static_for<1, N + 1>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int ml = N - j, nlo = tri_dim(ml);
+#pragma unroll
+      for (int k = 0; k < L::s3_slots(j); ++k) {
+        const int i = lane + 32 * k;
+        const bool ok = i < L::s3_items(j);
+        const int pi = ok ? i >> 1 : 0;
+        const int pw = pi / nlo, ii = pi - pw * nlo;
+        int b0, b1;
+        decode2(ml, ii, b0, b1);
+        const uint32_t v = (uint32_t)(2 * pw * (ml + 2) + 2 * b0) | ((uint32_t)(2 * b0) << 8);
+        const int x = L::s3_base(j) + k;
+        c3[x >> 1] |= v << (16 * (x & 1));
+      }
+    });
+  }
+  constexpr int SV1a = SV1 > 0 ? SV1 : 1;
+  uint32_t v1c[SV1a][2], v1w[SV1a];
+  T v1f[SV1a];
+#pragma unroll
+  for (int k = 0; k < SV1; ++k) {
+    const int i = ltid + GT * k;
+    const bool ok = i < KE * Npm;
+    const int e = ok ? i / Npm : 0, b = ok ? i - e * Npm : 0;
+    int b0, b1, b2;
+    decode3(N - 1, b, b0, b1, b2);
+    const int b3 = N - 1 - b0 - b1 - b2;
+    v1c[k][0] = pk(e * Np + pos3(N, b0 + 1, b1, b2), e * Np + pos3(N, b0, b1 + 1, b2));
+    v1c[k][1] = pk(e * Np + pos3(N, b0, b1, b2 + 1), e * Np + pos3(N, b0, b1, b2));
+    v1w[k] = pk(e * NWS + b, e);
+    v1f[k] = T(0.5 / (factorial(b0) * factorial(b1) * factorial(b2) * factorial(b3)));
+  }
+  uint32_t v2p[SV2][2], v2g[SV2][2], v2m[SV2];
+  T v2f[SV2];
+#pragma unroll
+  for (int k = 0; k < SV2; ++k) {
+    const int i = ltid + GT * k;
+    const bool ok = i < KE * Np;
+    const int e = ok ? i / Np : 0, a = ok ? i - e * Np : 0;
+    int a0, a1, a2;
+    decode3(N, a, a0, a1, a2);
+    const int al[4] = {a0, a1, a2, N - a0 - a1 - a2};
+    // V2 parents alpha - e_j in degree N-1 (lanes with alpha_j = 0 read the zero slot Npm)
+    const int q0 = al[0] ? pos3(N - 1, a0 - 1, a1, a2) : Npm, q1 = al[1] ? pos3(N - 1, a0, a1 - 1, a2) : Npm;
+    const int q2 = al[2] ? pos3(N - 1, a0, a1, a2 - 1) : Npm, q3 = al[3] ? pos3(N - 1, a0, a1, a2) : Npm;
+    v2p[k][0] = pk(e * NWS + q0, e * NWS + q1);
+    v2p[k][1] = pk(e * NWS + q2, e * NWS + q3);
+    uint32_t li[4];
+    for (int f = 0; f < 4; ++f) {
+      int bb[3], s = 0;
+      for (int v = 0; v < 4; ++v)
+        if (v != f) bb[s++] = al[v];
+      // (p, u) pair index of alpha in face f's cascade output
+      li[f] = 4 * KE * layer_off(N, al[f]) + (e * 4 + f) * tri_dim(N - al[f]) + pos2(N - al[f], bb[0], bb[1]);
+    }
+    v2g[k][0] = pk(li[0], li[1]);
+    v2g[k][1] = pk(li[2], li[3]);
+    v2m[k] = pk(ok ? i : 0, (e << 10) | a);
+    v2f[k] = T(factorial(al[0]) * factorial(al[1]) * factorial(al[2]) * factorial(al[3]));
+  }
+
+  // ---------------------------------------------------------------- staging
+  const int64_t fs = p.K * Np;
+  const T* __restrict__ q = p.q;
+  const int64_t ntiles = (p.kend - p.kbeg + KE - 1) / KE;
+  const int64_t stride = (int64_t)gridDim.x * NG;
+  int64_t tile = (int64_t)blockIdx.x * NG + g;
+  auto tile_k0 = [&](int64_t t) { return p.kbeg + t * KE; };
+  auto tile_nv = [&](int64_t t) {
+    const int64_t r = p.kend - tile_k0(t);
+    return (int)(r < KE ? r : KE);
+  };
+  // producer (lanes of the logical warp GW-1, one chunk each): TMA windows of the 4 state planes
+  // (+ res) and the geometry records.  Field F's window is placed so that its data starts at
+  // t_q + d0 + F S (d0 = (k0 Np) mod A); a window running past the array end leaves its last
+  // sub-16-byte piece to plain loads, written before the barrier arrive (release).
+  constexpr int NCH = L::RES ? 9 : 5;
+  auto issue_state = [&](int64_t k0, int nv, int st) {
+    T* s = stage_ptr(st);
+    uint64_t* bar = stage_bar(st);
+    const unsigned char* src = nullptr;
+    T* dst = nullptr;
+    uint32_t len = 0;
+    if (lane < NCH - 1) {
+      const int F = lane & 3;
+      const bool isq = lane < 4;
+      const int64_t g0 = k0 * Np;
+      const T* base = (isq ? q : p.res) + F * fs + g0;
+      const int dF = (int)(reinterpret_cast<uintptr_t>(base) & 15) / sz;   // = (F fs + g0) mod A
+      src = reinterpret_cast<const unsigned char*>(base - dF);
+      dst = s + (isq ? L::t_q : L::t_res) + (int)(g0 % A) + F * S - dF;
+      len = (uint32_t)((dF * sz + nv * Np * sz + 15) & ~15);
+      const unsigned char* end = reinterpret_cast<const unsigned char*>((isq ? q : p.res) + 4 * fs);
+      if (src + len > end) {
+        len -= 16;
+        const T* tb = reinterpret_cast<const T*>(src + len);
+        T* td = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(dst) + len);
+        for (const T* x = tb; reinterpret_cast<const unsigned char*>(x) < end; ++x) td[x - tb] = *x;
+      }
+    } else if (lane == NCH - 1) {
+      src = reinterpret_cast<const unsigned char*>(p.geo + k0 * kGeoRec);
+      dst = s + L::t_geo;
+      len = (uint32_t)(nv * kGeoRec * sz);
+    }
+    if (len) mbar_expect_tx_only(bar, len);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+    if (len) tma_bulk_g2s(dst, src, len, bar);
+  };
+  // neighbour face traces of tile (k0, nv): per face-point slot, 4 fields (cp.async)
+  int32_t ncode[SSa], nnbr[SSa];
+  auto load_conn = [&](int64_t k0, int nv) {
+#pragma unroll
+    for (int k = 0; k < SS; ++k) {
+      const int f = (s_ef[k] >> 8) & 3, e = s_ef[k] >> 10;
+      const int64_t kk = k0 + (e < nv ? e : 0);
+      ncode[k] = __ldg(p.code + kk);
+      nnbr[k] = __ldg(p.nbr + kk * 4 + f);
+    }
+  };
+  auto issue_nb = [&](int64_t k0, int nv, int st) {
+    const uint32_t sn = smem_u32(stage_ptr(st) + L::t_nb);
+    static_for<0, SS>([&](auto KK) {
+      constexpr int k = decltype(KK)::value;
+      slot<k, 32, NSI>(lane, [&] {
+        const int m = s_ef[k] & 0xff, f = (s_ef[k] >> 8) & 3, e = s_ef[k] >> 10;
+        if (e < nv) {
+          const int cd = (ncode[k] >> (8 * f)) & 0xff;
+          const bool bnd = cd & 32;
+          const T* src;
+          int64_t fstride = fs;
+          if (!(cd & 64)) {
+            // interior: neighbour's trace; boundary: own trace (the mirror sign lives in Bs)
+            const int key = bnd ? f * 6 : (cd & 3) * 6 + ((cd >> 2) & 7);
+            const int64_t k2 = bnd ? k0 + e : (int64_t)nnbr[k];
+            src = q + k2 * Np + tr2[key * Nfp + m];
+          } else {
+            src = p.halo + (int64_t)nnbr[k] * Nfp + ptab[((cd >> 2) & 7) * Nfp + m];
+            fstride = p.nhalo * Nfp;
+          }
+          const uint32_t d = sn + hi16(s_of[k]) * sz;
+#pragma unroll
+          for (int F = 0; F < 4; ++F) cp_async<sz>(d + F * NB * sz, src + F * fstride);
+        }
+      });
+    });
+  };
+
+  if (tile < ntiles) {
+    if (wg == L::GW - 1) issue_state(tile_k0(tile), tile_nv(tile), 0);
+    if constexpr (L::SURF) {
+      load_conn(tile_k0(tile), tile_nv(tile));
+      issue_nb(tile_k0(tile), tile_nv(tile), 0);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+  }
+  group_sync<GT>(g);
+
+  for (int it = 0; tile < ntiles; tile += stride, ++it) {
+    const int st = it & 1;
+    const int64_t k0 = tile_k0(tile);
+    const int nv = tile_nv(tile);
+    const int64_t tn = tile + stride;
+    const bool has_next = tn < ntiles;
+    const int64_t k0n = has_next ? tile_k0(tn) : 0;
+    const int nvn = has_next ? tile_nv(tn) : 0;
+    if (has_next) {
+      if (wg == L::GW - 1) {
+        fence_proxy_async();
+        issue_state(k0n, nvn, st ^ 1);
+      }
+      if constexpr (L::SURF) load_conn(k0n, nvn);
+    }
+    const T* stg = stage_ptr(st);
+    const T* sq = stg + L::t_q + (int)((k0 * Np) % A);   // field F at sq + F S; res at sq + RQ + F S
+    const T* sgeo = stg + L::t_geo;
+    const T* snb = stg + L::t_nb;
+    mbar_wait(stage_bar(st), (it >> 1) & 1);
+
+    // ------------------------------------------------------------- S1: upwind flux (solver.py:166-184)
+    if constexpr (L::SURF) {
+      static_for<0, SS>([&](auto KK) {
+        constexpr int k = decltype(KK)::value;
+        slot<k, 32, NSI>(lane, [&] {
+          const int own = lo16(s_of[k]), fl = hi16(s_of[k]);
+          const int f = (s_ef[k] >> 8) & 3, e = (KE == 1) ? 0 : (s_ef[k] >> 10);
+          const T* gr = sgeo + e * kGeoRec;
+          const V4<T> nf = *reinterpret_cast<const V4<T>*>(gr + 4 * f);
+          const T tp = gr[16 + 2 * f], cu = gr[17 + 2 * f];
+          T loc[4], nb[4];
+#pragma unroll
+          for (int F = 0; F < 4; ++F) {
+            loc[F] = sq[F * S + own];
+            nb[F] = snb[F * NB + fl];
+          }
+          const T bs = nf.w, ab = fabs(bs);
+          const T u = bs * nb[0] - ab * loc[0];   // |Bs| jp
+          const T jun = nf.x * (nb[1] - loc[1]) + nf.y * (nb[2] - loc[2]) + nf.z * (nb[3] - loc[3]);
+          sflux[fl] = P2<T>{tp * u - ab * jun, cu * jun - u};
+        });
+      });
+      __syncwarp();
+      if (has_next) issue_nb(k0n, nvn, st ^ 1);
+      cp_async_commit();
+
+      // ------------------------------------------------------------- S2: L0 (bernstein.py:221-229), scaled by b!
+      static_for<0, SS>([&](auto KK) {
+        constexpr int k = decltype(KK)::value;
+        slot<k, 32, NSI>(lane, [&] {
+          const int fl = hi16(s_of[k]), m = s_ef[k] & 0xff;
+          const int ef = s_ef[k] >> 8;
+          const V4<T> ca = l0c[m], cb = l0c[Nfp + m];
+          int o0, o1, o2, o3, o4, o5;
+          if constexpr (L::HOIST_L0) {
+            o0 = lo16(s_l0[k][0]), o1 = hi16(s_l0[k][0]), o2 = lo16(s_l0[k][1]), o3 = hi16(s_l0[k][1]);
+            o4 = lo16(s_l0[k][2]), o5 = hi16(s_l0[k][2]);
+          } else {
+            const uint4 lp = *reinterpret_cast<const uint4*>(sm + L::o_l0p + 16 * m);
+            const int fb = ef * NFS;
+            o0 = fb + lo16(lp.x), o1 = fb + hi16(lp.x), o2 = fb + lo16(lp.y), o3 = fb + hi16(lp.y);
+            o4 = fb + lo16(lp.z), o5 = fb + hi16(lp.z);
+          }
+          const P2<T> f0 = sflux[fl], f1 = sflux[o0], f2 = sflux[o1], f3 = sflux[o2], f4 = sflux[o3],
+                      f5 = sflux[o4], f6 = sflux[o5];
+          const T vp = ca.x * f0.x + ca.y * f1.x + ca.z * f2.x + ca.w * f3.x + cb.x * f4.x + cb.y * f5.x + cb.z * f6.x;
+          const T vu = ca.x * f0.y + ca.y * f1.y + ca.z * f2.y + ca.w * f3.y + cb.x * f4.y + cb.y * f5.y + cb.z * f6.y;
+          reinterpret_cast<P2<T>*>(sW)[ef * Nfp + m] = P2<T>{vp, vu};   // layer 0
+        });
+      });
+      // ------------------------------------------------------------- S3: reduction cascade (Alg. 1)
+      static_for<1, N + 1>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
+        const T kap = T(cascade_kappa(N, j));
+        T* const Bw = sW + 8 * KE * layer_off(N, j) + 2 * wg * PPW * nlo + lane;
+        const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
+        __syncwarp();
+        static_for<0, L::s3_slots(j)>([&](auto KK) {
+          constexpr int k = decltype(KK)::value;
+          constexpr int x = L::s3_base(j) + k;
+          slot<k, 32, L::s3_items(j)>(lane, [&] {
+            const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+            const T* rd = Br + 32 * k + (c & 0xff);
+            const T* r3 = rd - ((c >> 8) & 0xff);
+            Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
+          });
+        });
+      });
+    }
+
+    // ------------------------------------------------------------- V1: volume, degree N-1 half
+    if constexpr (L::VOL) {
+      static_for<0, SV1>([&](auto KK) {
+        constexpr int k = decltype(KK)::value;
+        slot<k, GT, KE * Npm>(ltid, [&] {
+          const int e = (KE == 1) ? 0 : (int)hi16(v1w[k]);
+          const T* gr = sgeo + e * kGeoRec;
+          const int c0 = lo16(v1c[k][0]), c1 = hi16(v1c[k][0]), c2 = lo16(v1c[k][1]), c3i = hi16(v1c[k][1]);
+          T d[4][3];
+#pragma unroll
+          for (int F = 0; F < 4; ++F) {
+            const T* qe = sq + F * S;
+            const T x0 = qe[c0], x1 = qe[c1], x2 = qe[c2], x3 = qe[c3i];
+            // children b+e_0..b+e_3: Delta_m = q[b+e_{m+1}] - q[b+e_0]  (exactly 0 for constant states)
+            d[F][0] = x1 - x0;
+            d[F][1] = x2 - x0;
+            d[F][2] = x3 - x0;
+          }
+          const T* G = gr + 26;   // rst_dx[m][i] = G[3m+i]
+          const T sr = -gr[25] * v1f[k];   // -(1/rho)/2 / beta!
+          const T sk = -gr[24] * v1f[k];   // -kappa/2 / beta!
+          T* w = sw + lo16(v1w[k]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            w[(1 + c) * KE * NWS] = sr * (G[c] * d[0][0] + G[3 + c] * d[0][1] + G[6 + c] * d[0][2]);
+          T div = T(0);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) div += G[c] * d[1 + c][0] + G[3 + c] * d[1 + c][1] + G[6 + c] * d[1 + c][2];
+          w[0] = sk * div;
+        });
+      });
+    }
+    group_sync<GT>(g);
+
+    // ------------------------------------------------------------- V2 + lift gather + epilogue
+    T* outF = p.out + k0 * Np;
+    T* resF = p.res + k0 * Np;
+    static_for<0, SV2>([&](auto KK) {
+      constexpr int k = decltype(KK)::value;
+      slot<k, GT, KE * Np>(ltid, [&] {
+        const int t = lo16(v2m[k]);
+        const int e = (KE == 1) ? 0 : (int)(hi16(v2m[k]) >> 10), a = hi16(v2m[k]) & 1023;
+        const T* gr = sgeo + e * kGeoRec;
+        (void)gr;
+        (void)a;
+        T r[4];
+        if constexpr (L::VOL) {
+          const int p0 = lo16(v2p[k][0]), p1 = hi16(v2p[k][0]), p2 = lo16(v2p[k][1]), p3 = hi16(v2p[k][1]);
+#pragma unroll
+          for (int F = 0; F < 4; ++F) {
+            const T* w = sw + F * KE * NWS;
+            r[F] = v2f[k] * ((w[p0] + w[p1]) + (w[p2] + w[p3]));
+          }
+        }
+        if constexpr (L::SURF) {
+          const int g0 = lo16(v2g[k][0]), g1 = hi16(v2g[k][0]), g2 = lo16(v2g[k][1]), g3 = hi16(v2g[k][1]);
+          const V4<T> gf = gfac[a];
+          const P2<T>* W2 = reinterpret_cast<const P2<T>*>(sW);
+          const P2<T> w0 = W2[g0], w1 = W2[g1], w2 = W2[g2], w3 = W2[g3];
+          const T sp = gf.x * w0.x + gf.y * w1.x + gf.z * w2.x + gf.w * w3.x;
+          const T u0 = gf.x * w0.y, u1 = gf.y * w1.y, u2 = gf.z * w2.y, u3 = gf.w * w3.y;
+          const V4<T> n0 = *reinterpret_cast<const V4<T>*>(gr + 0);
+          const V4<T> n1 = *reinterpret_cast<const V4<T>*>(gr + 4);
+          const V4<T> n2 = *reinterpret_cast<const V4<T>*>(gr + 8);
+          const V4<T> n3 = *reinterpret_cast<const V4<T>*>(gr + 12);
+          const T kap = gr[24], irho = gr[25];
+          const T s0 = kap * sp;
+          const T s1 = irho * (n0.x * u0 + n1.x * u1 + n2.x * u2 + n3.x * u3);
+          const T s2 = irho * (n0.y * u0 + n1.y * u1 + n2.y * u2 + n3.y * u3);
+          const T s3 = irho * (n0.z * u0 + n1.z * u1 + n2.z * u2 + n3.z * u3);
+          if constexpr (L::VOL) {
+            r[0] += s0;
+            r[1] += s1;
+            r[2] += s2;
+            r[3] += s3;
+          } else {
+            r[0] = s0;
+            r[1] = s1;
+            r[2] = s2;
+            r[3] = s3;
+          }
+        }
+        if (KE == 1 || (int)(hi16(v2m[k]) >> 10) < nv) {
+          if constexpr (OP == OP_STAGE) {
+            // res = A res + dt rhs; q_out = q_in + B res   (reference solver.py:211-213)
+#pragma unroll
+            for (int F = 0; F < 4; ++F) {
+              T x = sq[L::RQ + F * S + t] * p.rk_a;
+              x = x + p.dt * r[F];
+              const T qn = sq[F * S + t] + p.rk_b * x;
+              st_stream(resF + F * fs + t, x);
+              st_stream(outF + F * fs + t, qn);
+            }
+          } else {
+#pragma unroll
+            for (int F = 0; F < 4; ++F) {
+              T* o = outF + F * fs + t;
+              if (p.accumulate) *o = *o + r[F];
+              else st_stream(o, r[F]);
+            }
+          }
+        }
+      });
+    });
+    cp_async_wait_all();
+    group_sync<GT>(g);   // neighbour traces landed; this stage / work buffers free
+  }
+}
+
+}  // namespace bbdg

@@ -43,6 +43,7 @@ template <typename T> struct Params {
   T* res;                // (4,K,Np) LSRK register (OP_STAGE)
   const T* geo_vol;      // (K,12)
   const T* geo_surf;     // (K,24)
+  const T* geo;          // (K,36) fused record (bbdg_opt.cuh, kGeoRec)
   const int32_t* nbr;    // (K,4) neighbour element, or halo slot
   const int32_t* code;   // (K) 4 x int8: f2 | perm<<2 | boundary<<5 | halo<<6
   const T* halo;         // (4, nhalo, Nfp) remote traces in the sender's face order

@@ -3,17 +3,19 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--dtype f32|f64] [--n 26] [--orders 1-9] [--lift optimal]
 
-Workload (BASELINE.json configs[1]): cube_mesh(26) = 105,456 tets, Bernstein
-basis, orders N = 1..9, homogeneous materials, standard-normal synthetic
-state (seed 2024).  One bench "step" = one fused LSRK4 stage (volume +
-surface + update, ``bbdg_lsrk_stage``) at every order of the sweep; the
-headline value is the sweep's whole-job DOF throughput
-sum_N 4 K Np(N) / sum_N t_stage(N).  L2 (126 MB) is flushed with a 256 MB
-write before every timed launch, outside the event window.
+Workload (BASELINE.json configs[2], the kernel sweep): cube_mesh(40) =
+384,000 tets per GPU, Bernstein basis, orders N = 1..9, homogeneous
+materials, standard-normal synthetic state (seed 2024).  One bench "step" =
+one fused LSRK4 stage (volume + surface + update, ``bbdg_lsrk_stage``) at
+every order of the sweep; the headline value is the sweep's whole-job DOF
+throughput sum_N 4 K Np(N) / sum_N t_stage(N).  Orders run one after another
+(bounded memory); L2 (126 MB) is flushed with a 256 MB write before every
+timed launch, outside the event window.
 
 Per-order extras: volume / surface (3 lift modes) / update kernels timed
-separately, the nodal NPT comparison, and the roofline fraction of each
-against MEASURED_PEAKS.json.
+separately with their roofline fractions against MEASURED_PEAKS.json, the
+end-to-end lsrk4_step on a host state, and (configs[1]) the BB vs nodal
+comparison on cube_mesh(26).
 """
 
 from __future__ import annotations
@@ -140,7 +142,9 @@ def build_system(mesh, N, dtype, basis="bernstein"):
 
 
 def time_launches(torch, fn, flush, reps):
-    """Mean device time (ms) of fn over reps launches, L2 flushed before each (outside the events)."""
+    """Mean device time (ms) of fn over reps launches, L2 flushed before each (outside the events).
+    One untimed call first: the first launch of a kernel pays CUDA's lazy module load."""
+    fn()
     tot = 0.0
     for _ in range(reps):
         flush.zero_()
@@ -173,9 +177,9 @@ def run_ours(args, rank, world):
     K = mesh.K // world
     orders = parse_orders(args.orders)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    gen = torch.Generator(device="cuda").manual_seed(2024 + rank)
-    systems = {}
-    for N in orders:
+    peak, peak_kind = load_peaks()
+
+    def make_system(N):
         if world > 1:
             from paper_1512_06025_b200 import BernsteinRefOps, Materials
             from paper_1512_06025_b200.dist import DistWaveSystem
@@ -183,38 +187,75 @@ def run_ours(args, rank, world):
             sy = DistWaveSystem(mesh, BernsteinRefOps.build(N), Materials.homogeneous(mesh.K), dtype, rank, world,
                                 align=6 * args.n * args.n)
             sy.Np, sy.torch_dtype = sy.local.Np, sy.local.torch_dtype
-        else:
-            sy = build_system(mesh, N, dtype)
-        q = torch.randn((4, K, sy.Np), generator=gen, device="cuda", dtype=sy.torch_dtype)
-        systems[N] = dict(sy=sy, q=q, q2=torch.empty_like(q), res=torch.randn_like(q), rhs=torch.empty_like(q),
-                          dt=stable_dt(mesh, N, 1.0))
+            return sy
+        return build_system(mesh, N, dtype)
 
-    def stage(N):
-        d = systems[N]
-        d["sy"].stage_into(d["q"], d["q2"], d["res"], RK4A[1], RK4B[1], d["dt"], args.lift)
-
-    # warm-up
-    for _ in range(args.warmup):
-        for N in orders:
-            stage(N)
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-
-    # timed region: K steps, each one fused stage at every order, L2 flushed between launches
-    per_n = {N: 0.0 for N in orders}
+    # one order at a time (bounded memory): W warm-up stages, then K timed stages, each launch
+    # bracketed by CUDA events with the L2 flushed before it (outside the events)
+    per_n, rows = {}, {}
+    gen = torch.Generator(device="cuda").manual_seed(2024 + rank)
     with Clocks(dev) as clk:
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            for N in orders:
+        for N in orders:
+            sy = make_system(N)
+            q = torch.randn((4, K, sy.Np), generator=gen, device="cuda", dtype=sy.torch_dtype)
+            q2, res = torch.empty_like(q), torch.randn_like(q)
+            dt = stable_dt(mesh, N, 1.0)
+
+            def stage():
+                sy.stage_into(q, q2, res, RK4A[1], RK4B[1], dt, args.lift)
+
+            for _ in range(args.warmup):
+                stage()
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            tot = 0.0
+            for _ in range(args.steps):
                 flush.zero_()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                stage(N)
+                stage()
                 b.record()
                 b.synchronize()
-                per_n[N] += a.elapsed_time(b)
-        torch.cuda.synchronize()
+                tot += a.elapsed_time(b)
+            torch.cuda.synchronize()
+            per_n[N] = tot
+            t_stage = tot / args.steps
+            ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9
+            row = {"gdofs_stage": 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
+                   "stage_gbs": ach, "stage_frac": ach / peak}
+            if not args.quick and world == 1:
+                rhs = torch.empty_like(q)
+                reps = max(3, args.steps)
+                tv = time_launches(torch, lambda: sy.volume_into(q, rhs), flush, reps)
+                row["volume_ms"], row["volume_frac"] = tv, volume_bytes(N, s, K) / (tv * 1e-3) / 1e9 / peak
+                for mode in ("factorized", "optimal", "dense"):
+                    ts = time_launches(torch, lambda: sy.surface_into(q, rhs, mode), flush, reps)
+                    row[f"surface_{mode}_ms"] = ts
+                    row[f"surface_{mode}_frac"] = surface_bytes(N, s, K) / (ts * 1e-3) / 1e9 / peak
+                from paper_1512_06025_b200.solver import _device_update
+                tu = time_launches(torch, lambda: _device_update(q2, res, rhs, RK4A[1], RK4B[1], dt), flush, reps)
+                row["update_ms"], row["update_frac"] = tu, update_bytes(N, s, K) / (tu * 1e-3) / 1e9 / peak
+                row["unfused_gdofs"] = 4 * K * np_of(N) / ((tv + row["surface_optimal_ms"] + tu) * 1e-3) / 1e9
+                del rhs
+            if world == 1:
+                # end to end through the public API with a pinned host state: H2D + 5 stages + D2H
+                host = torch.empty((4, K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
+                host.copy_(q)
+                st = FieldState(host.numpy(), "bernstein")
+                lsrk4_step(sy, st, dt, args.lift)   # warm
+                torch.cuda.synchronize()
+                reps = 2 if args.quick else max(2, min(args.steps, 5))
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    lsrk4_step(sy, st, dt, args.lift)
+                torch.cuda.synchronize()
+                row["e2e_ms_step"] = (time.perf_counter() - t0) * 1e3 / reps
+                row["e2e_bytes"] = 2 * host.numel() * host.element_size()
+                del host, st
+            rows[str(N)] = row
+            del sy, q, q2, res
+            torch.cuda.empty_cache()
     total_ms = sum(per_n.values())
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
@@ -223,80 +264,59 @@ def run_ours(args, rank, world):
         torch.distributed.barrier()
     dofs_per_step = sum(4 * K * np_of(N) for N in orders)
     value = world * dofs_per_step * args.steps / (total_ms * 1e-3) / 1e9
-
-    peak, peak_kind = load_peaks()
-    out = dict(per_order={}, value=value, ms_per_step=total_ms / args.steps, clocks=clk.summary())
-    # per-order stage rooflines + kernel breakdown (outside the headline timing)
-    dominant = None
-    for N in orders:
-        d = systems[N]
-        t_stage = per_n[N] / args.steps
-        bytes_ = stage_bytes(N, s, K)
-        ach = bytes_ / (t_stage * 1e-3) / 1e9
-        row = {"gdofs_stage": 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
-               "stage_gbs": ach, "stage_frac": ach / peak}
-        if not args.quick and world == 1:
-            sy, q, rhs = d["sy"], d["q"], d["rhs"]
-            reps = max(3, args.steps)
-            tv = time_launches(torch, lambda: sy.volume_into(q, rhs), flush, reps)
-            row["volume_ms"], row["volume_frac"] = tv, volume_bytes(N, s, K) / (tv * 1e-3) / 1e9 / peak
-            for mode in ("factorized", "optimal", "dense"):
-                ts = time_launches(torch, lambda: sy.surface_into(q, rhs, mode), flush, reps)
-                row[f"surface_{mode}_ms"] = ts
-                row[f"surface_{mode}_frac"] = surface_bytes(N, s, K) / (ts * 1e-3) / 1e9 / peak
-            from paper_1512_06025_b200.solver import _device_update
-            tu = time_launches(torch, lambda: _device_update(d["q2"], d["res"], rhs, RK4A[1], RK4B[1], d["dt"]),
-                               flush, reps)
-            row["update_ms"], row["update_frac"] = tu, update_bytes(N, s, K) / (tu * 1e-3) / 1e9 / peak
-            row["unfused_gdofs"] = 4 * K * np_of(N) / ((tv + row["surface_optimal_ms"] + tu) * 1e-3) / 1e9
-            if N <= 9 and args.nodal:
-                sn = build_system(mesh, N, dtype, "nodal")
-                qn, rn = torch.randn_like(q), torch.empty_like(q)
-                tn = time_launches(torch, lambda: sn.rhs_into(qn, rn, "dense"), flush, max(2, reps // 2))
-                row["nodal_npt_rhs_ms"] = tn
-                row["bb_over_nodal_rhs"] = tn / time_launches(torch, lambda: sy.rhs_into(q, rhs, args.lift), flush,
-                                                              reps)
-                del sn
-        out["per_order"][str(N)] = row
-        if dominant is None or per_n[N] > per_n[dominant]:
-            dominant = N
-    Nd = dominant
+    out = dict(per_order=rows, value=value, ms_per_step=total_ms / args.steps, clocks=clk.summary())
+    Nd = max(orders, key=lambda N: per_n[N])   # dominant kernel: the order with the largest stage time
     t_d = per_n[Nd] / args.steps
     ach = stage_bytes(Nd, s, K) / (t_d * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(args.dtype, {}).get(str(Nd))
+        traffic = json.loads(tp.read_text()).get(args.dtype, {}).get(f"n{args.n}", {}).get(str(Nd))
     out["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                       "traffic": traffic, "kernel": f"tile_kernel<{args.dtype},N={Nd},OP_STAGE,{args.lift}>",
-                       "peak_kind": peak_kind,
-                       "bytes_per_launch": stage_bytes(Nd, s, K)}
+                       "traffic": traffic, "kernel": f"opt_kernel<{args.dtype},N={Nd},OP_STAGE> ({args.lift} lift)",
+                       "peak_kind": peak_kind, "bytes_per_launch": stage_bytes(Nd, s, K)}
     out["gpu_launches"] = args.steps * len(orders)
-
-    # end-to-end through the public API with host (numpy) buffers
-    e2e_ms, h2d, d2h = 0.0, 0, 0
-    e2e_reps = 2 if args.quick else max(2, min(args.steps, 5))
-    for N in (orders if world == 1 else []):
-        d = systems[N]
-        host = torch.empty((4, K, d["sy"].Np), dtype=d["sy"].torch_dtype, pin_memory=True)
-        host.copy_(d["q"])
-        hq = host.numpy()
-        st = FieldState(hq, "bernstein")
-        lsrk4_step(d["sy"], st, d["dt"], args.lift)  # warm
-        torch.cuda.synchronize()
-        for _ in range(e2e_reps):
-            t0 = time.perf_counter()
-            lsrk4_step(d["sy"], st, d["dt"], args.lift)
-            torch.cuda.synchronize()
-            e2e_ms += (time.perf_counter() - t0) * 1e3
-        h2d += hq.nbytes
-        d2h += hq.nbytes
-    e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders) * e2e_reps
-    out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9 if e2e_ms else None, "unit": UNIT,
-                  "h2d_bytes_per_step": h2d,
-                  "d2h_bytes_per_step": d2h,
-                  "what": "lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"}
+    if world == 1:
+        e2e_ms = sum(r["e2e_ms_step"] for r in rows.values())
+        e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders)
+        out["e2e"] = {"value": e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+                      "h2d_bytes_per_step": sum(r["e2e_bytes"] // 2 for r in rows.values()),
+                      "d2h_bytes_per_step": sum(r["e2e_bytes"] // 2 for r in rows.values()),
+                      "what": "lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"}
+    else:
+        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                      "what": "not measured for N > 1 (the public single-process API is the 1-GPU path)"}
+    if world == 1 and args.nodal and not args.quick:
+        out["comparison"] = compare_bases(args, dtype, flush)
     return out, K
+
+
+def compare_bases(args, dtype, flush):
+    """configs[1]: BB (fused stage / rhs) vs nodal DG rhs -- node-per-thread dense (paper NPT) and
+    block-partitioned tensor-core (paper EPT) -- on cube_mesh(26), per order."""
+    import torch
+
+    from paper_1512_06025_b200 import cube_mesh
+    from paper_1512_06025_b200.solver import RK4A, RK4B
+
+    mesh = cube_mesh(26)
+    out = {"mesh": f"cube_mesh(26) K={mesh.K}", "per_order": {}}
+    for N in parse_orders(args.orders):
+        sb, sn = build_system(mesh, N, dtype), build_system(mesh, N, dtype, "nodal")
+        q = torch.randn((4, mesh.K, sb.Np), device="cuda", dtype=sb.torch_dtype)
+        q2, res, rhs = torch.empty_like(q), torch.randn_like(q), torch.empty_like(q)
+        reps = 3
+        tb = time_launches(torch, lambda: sb.rhs_into(q, rhs, args.lift), flush, reps)
+        ts = time_launches(torch, lambda: sb.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, args.lift), flush, reps)
+        tn = time_launches(torch, lambda: sn.rhs_into(q, rhs, "dense"), flush, reps)
+        tk = time_launches(torch, lambda: sn.rhs_into(q, rhs, "blocked"), flush, reps)
+        flops = 2 * mesh.K * 4 * (3 * sb.Np ** 2 + sb.Np * 4 * sb.ops.Nfp)   # useful nodal GEMM flops
+        out["per_order"][str(N)] = {"bb_rhs_ms": tb, "bb_stage_ms": ts, "nodal_npt_rhs_ms": tn,
+                                    "nodal_blocked_rhs_ms": tk, "nodal_blocked_tflops": flops / tk / 1e9,
+                                    "bb_over_nodal_npt": tn / tb, "bb_over_nodal_blocked": tk / tb}
+        del sb, sn, q, q2, res, rhs
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------- CPU arm (oracle port)
@@ -333,7 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--n", type=int, default=26, help="cube_mesh(n): K = 6 n^3")
+    ap.add_argument("--n", type=int, default=40, help="cube_mesh(n): K = 6 n^3 per GPU")
     ap.add_argument("--orders", default="1-9")
     ap.add_argument("--lift", default="optimal", choices=["optimal", "factorized", "dense"])
     ap.add_argument("--cpu-n", type=int, default=8, help="oracle sample mesh cube_mesh(cpu_n)")
@@ -389,6 +409,8 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (standard normal, seed 2024)",
             "config": config, "roofline": out["roofline"], "e2e": out["e2e"], "gpu_launches": out["gpu_launches"],
             "clocks": out["clocks"], "per_order": out["per_order"]}
+    if "comparison" in out:
+        line["comparison"] = out["comparison"]
     if not args.no_cpu_baseline:
         v, Ks, t = cpu_sweep(orders, args.cpu_n, dtype)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",

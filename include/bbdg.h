@@ -28,8 +28,11 @@ typedef enum {
 
 enum { BBDG_BASIS_BERNSTEIN = 0, BBDG_BASIS_NODAL = 1 };
 enum { BBDG_F32 = 0, BBDG_F64 = 1 };
-/* lift modes of BernsteinRefOps.lift_flux (bernstein.py:457-466); nodal is always dense */
-enum { BBDG_LIFT_FACTORIZED = 0, BBDG_LIFT_OPTIMAL = 1, BBDG_LIFT_DENSE = 2 };
+/* lift modes of BernsteinRefOps.lift_flux (bernstein.py:457-466).  The nodal basis runs the
+ * reference's dense path (nodal.py:236-241) either as node-per-thread kernels (DENSE, paper
+ * "NPT") or as block-partitioned tensor-core GEMMs with a fused chain-rule/lift epilogue
+ * (BLOCKED, paper "EPT": fp64 DMMA, fp32 3xTF32); BLOCKED is nodal-only. */
+enum { BBDG_LIFT_FACTORIZED = 0, BBDG_LIFT_OPTIMAL = 1, BBDG_LIFT_DENSE = 2, BBDG_LIFT_BLOCKED = 3 };
 
 typedef struct bbdg_ctx bbdg_ctx;
 

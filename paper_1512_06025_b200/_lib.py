@@ -14,7 +14,7 @@ LIB_PATH = Path(os.environ.get("BBDG_LIB") or Path(__file__).resolve().parent / 
 
 BASIS = {"bernstein": 0, "nodal": 1}
 DTYPE = {"float32": 0, "float64": 1}
-LIFT = {"factorized": 0, "optimal": 1, "dense": 2}
+LIFT = {"factorized": 0, "optimal": 1, "dense": 2, "blocked": 3}   # blocked: nodal tensor-core path
 OP = {"volume": 0, "surface": 1, "rhs": 2, "stage": 3}
 
 _P = C.c_void_p

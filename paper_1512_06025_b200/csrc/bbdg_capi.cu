@@ -7,6 +7,7 @@
 
 #include "bbdg_common.cuh"
 #include "bbdg_internal.h"
+#include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
 
 struct bbdg_ctx {
@@ -24,6 +25,9 @@ struct bbdg_ctx {
   int el_w = 0;
   void* liftT = nullptr;     // T (4Nfp,Np)
   void* dT = nullptr;        // T (3,Np,Np)
+  void* bvol = nullptr;      // nodal blocked: D_m^T MMA fragments
+  void* blift = nullptr;     // nodal blocked: L^T MMA fragments
+  void* flux = nullptr;      // nodal blocked: (4, K, 4 Nfp) face-flux scratch
   const void* halo = nullptr;
   int64_t nhalo = 0;
 };
@@ -127,6 +131,47 @@ static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa
   c->nbr = static_cast<int32_t*>(upload(nb, &rc));
   c->code = static_cast<int32_t*>(upload(cd, &rc));
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// nodal blocked path: operator fragments in mma.sync lane order (bbdg_nodal.cuh)
+// ---------------------------------------------------------------------------
+// round-to-nearest (ties away) to tf32, as cvt.rna.tf32.f32
+static float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// B(k, n) = Mats[m][n * kdim + k] (operator rows n = output node), per (m, k-step, n-tile, lane)
+template <typename T>
+static std::vector<T> mma_fragments(const double* const* mats, int nm, int Np, int kdim) {
+  using MM = NodalMma<T>;
+  const int KS = MM::KS, NT = MM::NT, nks = (kdim + KS - 1) / KS, ntl = (Np + NT - 1) / NT;
+  const int per = sizeof(T) == 4 ? 4 : 1;
+  std::vector<T> out((size_t)nm * nks * ntl * 32 * per, T(0));
+  for (int m = 0; m < nm; ++m)
+    for (int ks = 0; ks < nks; ++ks)
+      for (int nt = 0; nt < ntl; ++nt)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int g = lane >> 2, t = lane & 3, n = nt * NT + g;
+          auto B = [&](int k) { return (n < Np && k < kdim) ? mats[m][(size_t)n * kdim + k] : 0.0; };
+          T* o = &out[((((size_t)m * nks + ks) * ntl + nt) * 32 + lane) * per];
+          if constexpr (sizeof(T) == 4) {
+            const float b0 = (float)B(ks * KS + t), b1 = (float)B(ks * KS + t + 4);
+            const float h0 = tf32_rna(b0), h1 = tf32_rna(b1);
+            o[0] = h0;
+            o[1] = h1;
+            o[2] = tf32_rna(b0 - h0);
+            o[3] = tf32_rna(b1 - h1);
+          } else {
+            o[0] = (T)B(ks * KS + t);
+          }
+        }
+  return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -235,6 +280,9 @@ template <typename T> static Params<T> make_params(const bbdg_ctx* c) {
   p.el_w = c->el_w;
   p.liftT = static_cast<const T*>(c->liftT);
   p.dT = static_cast<const T*>(c->dT);
+  p.flux = static_cast<T*>(c->flux);
+  p.bvol = c->bvol;
+  p.blift = c->blift;
   return p;
 }
 
@@ -250,13 +298,19 @@ static int check_ctx(const bbdg_ctx* c) {
 
 static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
   if (c->basis == BBDG_BASIS_NODAL) {
-    // WaveSystem forces "dense" for the nodal basis (solver.py:168-169)
+    // WaveSystem forces "dense" for the nodal basis (solver.py:168-169); BLOCKED selects the
+    // tensor-core (EPT) kernels for the same arithmetic
+    if (lift == BBDG_LIFT_BLOCKED) {
+      if (!c->bvol || !c->blift || !c->flux)
+        return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded (set_nodal_ops + set_lift_tables)");
+      return BBDG_OK;
+    }
     lift = BBDG_LIFT_DENSE;
     if (surf && !c->liftT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal dense lift not uploaded");
     if (!c->dT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal derivative matrices not uploaded");
     return BBDG_OK;
   }
-  if (lift < 0 || lift > 2) return set_error(BBDG_ERR_ARG, "unknown lift mode");
+  if (lift < 0 || lift > 2) return set_error(BBDG_ERR_ARG, "unknown lift mode (blocked is nodal-only)");
   if (surf && lift == BBDG_LIFT_FACTORIZED && !c->el_vals)
     return set_error(BBDG_ERR_UNSUPPORTED, "E_L table not uploaded (bbdg_ctx_set_lift_tables)");
   if (surf && lift == BBDG_LIFT_DENSE && !c->liftT)
@@ -307,6 +361,9 @@ void bbdg_ctx_destroy(bbdg_ctx* c) {
   cudaFree(c->el_cols);
   cudaFree(c->liftT);
   cudaFree(c->dT);
+  cudaFree(c->bvol);
+  cudaFree(c->blift);
+  cudaFree(c->flux);
   delete c;
 }
 
@@ -347,6 +404,19 @@ int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* 
     cudaFree(c->liftT);
     c->liftT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
                                     : upload(cast<double>(t.data(), t.size()), &rc);
+    if (c->basis == BBDG_BASIS_NODAL) {
+      const double* m[1] = {dense_L};
+      cudaFree(c->blift);
+      cudaFree(c->flux);
+      c->blift = c->dtype == BBDG_F32 ? upload(mma_fragments<float>(m, 1, Np, 4 * Nfp), &rc)
+                                      : upload(mma_fragments<double>(m, 1, Np, 4 * Nfp), &rc);
+      const size_t fb = (size_t)4 * c->K * 4 * Nfp * (c->dtype == BBDG_F32 ? 4 : 8);
+      cudaError_t e = cudaMalloc(&c->flux, std::max<size_t>(fb, 16));
+      if (e != cudaSuccess) {
+        c->flux = nullptr;
+        rc = set_cuda_error(e, "nodal flux scratch");
+      }
+    }
   }
   return rc;
 }
@@ -363,6 +433,9 @@ int bbdg_ctx_set_nodal_ops(bbdg_ctx* c, const double* Dr, const double* Ds, cons
   cudaFree(c->dT);
   c->dT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
                                : upload(cast<double>(t.data(), t.size()), &rc);
+  cudaFree(c->bvol);
+  c->bvol = c->dtype == BBDG_F32 ? upload(mma_fragments<float>(D, 3, Np, Np), &rc)
+                                 : upload(mma_fragments<double>(D, 3, Np, Np), &rc);
   return rc;
 }
 

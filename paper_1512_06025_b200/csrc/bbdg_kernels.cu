@@ -2,6 +2,7 @@
 // dtype combinations build in parallel.  Exposes a launcher table entry
 // through a C++ symbol named after the pair.
 #include "bbdg_internal.h"
+#include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
 
 #ifndef BBDG_T
@@ -45,9 +46,37 @@ template <int OP, int FSR> int launch_opt(const void* vp, cudaStream_t stream, i
       opt_kernel<T, BBDG_N, OP, FSR>, blocks_per_sm, vp, stream, num_sms);
 }
 
+// nodal block-partitioned path: flux kernel (surface ops), then the tensor-core GEMM kernel
+template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_sms) {
+  using T = BBDG_T;
+  using L = NodalLayout<T, BBDG_N>;
+  const Params<T>& p = *static_cast<const Params<T>*>(vp);
+  const int64_t nl = p.kend - p.kbeg;
+  if (nl == 0) return BBDG_OK;
+  if (!p.bvol || !p.blift || !p.flux) return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded");
+  if constexpr (OP != OP_VOLUME) {
+    const int64_t n = nl * 4 * Dims<BBDG_N>::Nfp;
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 8);
+    nodal_flux_kernel<T, BBDG_N><<<(unsigned)grid, 256, 0, stream>>>(p);
+  }
+  static bool attr = false;
+  auto kern = nodal_mma_kernel<T, BBDG_N, OP>;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal)");
+    attr = true;
+  }
+  const int64_t ntiles = (nl + NodalMma<T>::MT - 1) / NodalMma<T>::MT;
+  kern<<<(unsigned)std::min<int64_t>(ntiles, num_sms), L::THREADS, L::total, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal MMA kernel launch");
+}
+
 template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t stream, int num_sms) {
   using T = BBDG_T;
-  if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) {
+  if constexpr (BASIS == BASIS_NODAL && LIFT == LIFT_BLOCKED) {
+    return launch_nodal<OP>(vp, stream, num_sms);
+  } else if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) {
     // field-plane stride residue (K Np) mod (16 / sizeof(T)) selects the smem field stride
     const Params<T>& p = *static_cast<const Params<T>*>(vp);
     constexpr int A = 16 / sizeof(T);
@@ -71,7 +100,8 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
 }
 
 template <int OP, int LIFT, int BASIS> int64_t smem() {
-  if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) return OptLayout<BBDG_T, BBDG_N, OP, 0>::total;
+  if constexpr (BASIS == BASIS_NODAL && LIFT == LIFT_BLOCKED) return NodalLayout<BBDG_T, BBDG_N>::total;
+  else if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) return OptLayout<BBDG_T, BBDG_N, OP, 0>::total;
   else return Layout<BBDG_T, BBDG_N, OP, LIFT, BASIS>::total;
 }
 
@@ -102,6 +132,10 @@ KernelEntry BBDG_CAT(entry, BBDG_TNAME, BBDG_N)(int op, int lift, int basis) {
   BBDG_CASE(OP_SURFACE, LIFT_DENSE, BASIS_NODAL)
   BBDG_CASE(OP_RHS, LIFT_DENSE, BASIS_NODAL)
   BBDG_CASE(OP_STAGE, LIFT_DENSE, BASIS_NODAL)
+  BBDG_CASE(OP_VOLUME, LIFT_BLOCKED, BASIS_NODAL)
+  BBDG_CASE(OP_SURFACE, LIFT_BLOCKED, BASIS_NODAL)
+  BBDG_CASE(OP_RHS, LIFT_BLOCKED, BASIS_NODAL)
+  BBDG_CASE(OP_STAGE, LIFT_BLOCKED, BASIS_NODAL)
 #undef BBDG_CASE
   return k;
 }

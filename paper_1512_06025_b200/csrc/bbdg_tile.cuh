@@ -29,7 +29,7 @@
 namespace bbdg {
 
 enum Op : int { OP_VOLUME = 0, OP_SURFACE = 1, OP_RHS = 2, OP_STAGE = 3 };
-enum Lift : int { LIFT_FACTORIZED = 0, LIFT_OPTIMAL = 1, LIFT_DENSE = 2 };
+enum Lift : int { LIFT_FACTORIZED = 0, LIFT_OPTIMAL = 1, LIFT_DENSE = 2, LIFT_BLOCKED = 3 };
 enum Basis : int { BASIS_BERNSTEIN = 0, BASIS_NODAL = 1 };
 
 constexpr int kGeoVol = 12;   // rst_dx[m][i] (9), kappa, inv_rho, pad
@@ -55,6 +55,9 @@ template <typename T> struct Params {
   const T* dT;           // nodal (3, Np, Np): dT[d][b][a] = D_d[a][b]
   T rk_a, rk_b, dt;
   int accumulate;
+  T* flux;               // nodal blocked path: (4, kend - kbeg, 4 Nfp) face fluxes (context-owned)
+  const void* bvol;      // nodal blocked path: D_m^T MMA fragments (bbdg_nodal.cuh)
+  const void* blift;     // nodal blocked path: L^T MMA fragments
 };
 
 template <typename T> struct alignas(4 * sizeof(T)) V4 {

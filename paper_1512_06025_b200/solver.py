@@ -275,10 +275,18 @@ class WaveSystem:
         self.volume_into(q, dq)
         return self._out(dq, state.q)
 
+    def _nodal_mode(self, lift_mode):
+        """The reference forces "dense" for the nodal basis (solver.py:168-169); "blocked" picks the
+        block-partitioned tensor-core kernels for the same arithmetic."""
+        if self.basis == "nodal":
+            return "blocked" if lift_mode == "blocked" else "dense"
+        if lift_mode == "blocked":
+            raise ValueError("lift mode 'blocked' is nodal-only")
+        return lift_mode
+
     def surface_rhs(self, state: FieldState, lift_mode: str = "factorized"):
         self._check(state)
-        if self.basis == "nodal":
-            lift_mode = "dense"
+        lift_mode = self._nodal_mode(lift_mode)
         self._lift_id(lift_mode)
         q = self.to_device(state.q)
         dq = self._torch.empty_like(q)
@@ -287,8 +295,7 @@ class WaveSystem:
 
     def rhs(self, state: FieldState, lift_mode: str = "factorized"):
         self._check(state)
-        if self.basis == "nodal":
-            lift_mode = "dense"
+        lift_mode = self._nodal_mode(lift_mode)
         self._lift_id(lift_mode)
         q = self.to_device(state.q)
         dq = self._torch.empty_like(q)
@@ -332,7 +339,7 @@ def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorize
     t0 = state.time
     if isinstance(system, WaveSystem):
         system._check(state)
-        lift = "dense" if system.basis == "nodal" else lift_mode
+        lift = system._nodal_mode(lift_mode)
         system._lift_id(lift)
         q = system.to_device(state.q)
         r = system.to_device(res) if res is not None else torch.empty_like(q)
@@ -381,7 +388,7 @@ def integrate(system, state: FieldState, dt: float, nsteps: int, lift_mode: str 
         raise ValueError("dt must be positive")
     system._check(state)
     torch = _torch()
-    lift = "dense" if system.basis == "nodal" else lift_mode
+    lift = system._nodal_mode(lift_mode)
     system._lift_id(lift)
     host = not _is_tensor(state.q)
     bufs = [system.to_device(state.q), None]

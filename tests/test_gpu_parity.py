@@ -76,6 +76,35 @@ def test_nodal_parity_with_reference_golden(golden_nodal, N):
     assert rel_l2(st.q, g[f"N{N}_step"]) < TOL["f64"]
 
 
+@pytest.mark.parametrize("N", range(1, 7))
+@pytest.mark.parametrize("dname", ["f64", "f32"])
+def test_nodal_blocked_parity_with_reference_golden(golden_nodal, N, dname):
+    """Block-partitioned tensor-core nodal kernels (fp64 DMMA, fp32 3xTF32) vs the reference."""
+    g = golden_nodal
+    m = cube_mesh(2)
+    sy = WaveSystem(m, NodalRefOps.build(N), Materials.homogeneous(m.K), dtype=DT[dname])
+    q = g[f"N{N}_q"].astype(DT[dname])
+    assert rel_l2(sy.rhs(FieldState(q.copy(), "nodal"), "blocked"), g[f"N{N}_rhs"]) < TOL[dname]
+    st = lsrk4_step(sy, FieldState(q.copy(), "nodal"), float(g[f"N{N}_dt"]), "blocked")
+    assert rel_l2(st.q, g[f"N{N}_step"]) < TOL[dname]
+
+
+@pytest.mark.parametrize("N", [2, 7, 9])
+@pytest.mark.parametrize("dname", ["f64", "f32"])
+def test_nodal_blocked_matches_dense_fresh_inputs(N, dname):
+    """K = 162 (partial element tiles), heterogeneous materials: blocked vs the NPT dense kernels
+    (which are pinned to the reference golden vectors above)."""
+    m = cube_mesh(3)
+    rng = np.random.default_rng(7 + N)
+    mat = Materials(rng.uniform(0.5, 2.0, m.K), rng.uniform(0.5, 2.0, m.K))
+    sd = WaveSystem(m, NodalRefOps.build(N), mat, dtype=np.float64)
+    sb = WaveSystem(m, NodalRefOps.build(N), mat, dtype=DT[dname])
+    q = rng.standard_normal((4, m.K, sd.Np))
+    want = sd.rhs(FieldState(q.copy(), "nodal"))
+    got = sb.rhs(FieldState(q.astype(DT[dname]), "nodal"), "blocked")
+    assert rel_l2(got, want) < TOL[dname]
+
+
 @pytest.mark.parametrize("N", [1, 3, 5, 7, 9])
 @pytest.mark.parametrize("dname", ["f64", "f32"])
 def test_bb_parity_with_oracle_fresh_inputs(N, dname):

@@ -106,6 +106,19 @@ int bbdg_step(bbdg_ctx* ctx, void* q, void* q_tmp, void* res, double dt, int lif
  * sendbuf (4, n, Nfp) in each face's own canonical order (halo send side). */
 int bbdg_halo_pack(bbdg_ctx* ctx, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream);
 
+/* Device-resident functionals (float64 results written to device memory `out`; `partial`
+ * is caller-owned (K) float64 scratch; deterministic fixed-order reductions).
+ * discrete_energy (solver.py:306-312): out = sum_k sum_F coef[F][k] q_F^T M q_F with the
+ *   symmetric mass matrix M (Np, Np) and coef (4, K) = (J/kappa, J rho, J rho, J rho).
+ * ErrorFunctional (solver.py:282-296): out = sqrt(sum_k jac_k sum_i w_i (E q_0 - p_exact)^2)
+ *   with eval_t = E^T (Np, nq), barycentric quadrature points lam (nq, 4), element
+ *   vertices (K, 4, 3) and the standing wave p_exact of exact_solution (solver.py:249-261). */
+int bbdg_energy(int dtype, int64_t K, int Np, const void* q, const double* mass, const double* coef,
+                double* partial, double* out, void* stream);
+int bbdg_error_l2(int dtype, int64_t K, int Np, int nq, const void* q0, const double* eval_t, const double* wq,
+                  const double* lam, const double* verts, const double* jac, double tau, double* partial,
+                  double* out, void* stream);
+
 /* Introspection used by tests and the benchmark. */
 int bbdg_tile_elems(int N, int dtype);
 int64_t bbdg_kernel_smem(int N, int dtype, int op, int lift, int basis);

@@ -47,7 +47,7 @@ def _sources_digest() -> str:
 
 
 def _units():
-    units = [("bbdg_capi", CSRC / "bbdg_capi.cu", [])]
+    units = [("bbdg_capi", CSRC / "bbdg_capi.cu", []), ("bbdg_func", CSRC / "bbdg_func.cu", [])]
     for tname, t in (("f32", "float"), ("f64", "double")):
         for n in range(1, MAX_DEGREE + 1):
             units.append((f"k_{tname}_{n}", CSRC / "bbdg_kernels.cu",
@@ -60,7 +60,7 @@ def build_variant(out_dir: Path, defines: list[str], dtypes=("f32",), jobs: int 
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
     exe = nvcc()
-    units = [u for u in _units() if u[0] == "bbdg_capi" or u[0].split("_")[1] in dtypes]
+    units = [u for u in _units() if not u[0].startswith("k_") or u[0].split("_")[1] in dtypes]
     missing = [u for u in _units() if u not in units]
 
     def compile_unit(u):

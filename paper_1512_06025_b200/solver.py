@@ -450,16 +450,52 @@ def initial_state(mesh: Mesh, N: int, basis: str, dtype=np.float64, node_kind: s
 
 
 class ErrorFunctional:
-    """Quadrature of (p_h - p)^2 with a degree 2N+2 rule (solver.py:282-296)."""
+    """Quadrature of (p_h - p)^2 with a degree 2N+2 rule (solver.py:282-296).
+
+    Device states are evaluated by the bbdg_error_l2 kernel (no host copy); numpy
+    states by the same float64 arithmetic on the host, as the reference does."""
 
     def __init__(self, mesh: Mesh, ops):
         pts, w = tet_rule(2 * ops.N + 2)
         self.w = w
+        self.pts = pts
+        self.mesh = mesh
         self.phys = mesh.map_reference_points(pts)
         self.E = ops.eval_matrix(pts)
         self.jac = mesh.jac
+        self._dev = None
+
+    def _device_arrays(self, device):
+        if self._dev is None:
+            torch = _torch()
+            from .multiindex import barycentric_from_rst
+
+            f64 = dict(dtype=torch.float64, device=device)
+            self._dev = dict(
+                ET=torch.as_tensor(np.ascontiguousarray(self.E.T), **f64),
+                w=torch.as_tensor(np.ascontiguousarray(self.w), **f64),
+                lam=torch.as_tensor(np.ascontiguousarray(barycentric_from_rst(self.pts)), **f64),
+                verts=torch.as_tensor(np.ascontiguousarray(self.mesh.element_vertices()), **f64),
+                jac=torch.as_tensor(np.ascontiguousarray(self.jac), **f64),
+                partial=torch.empty(len(self.jac), **f64), out=torch.empty(1, **f64))
+        return self._dev
+
+    def device(self, q, tau: float) -> float:
+        """Error of a device state q (4, K, Np) at time tau (one D2H of 8 bytes)."""
+        torch = _torch()
+        d = self._device_arrays(q.device)
+        K, Np = q.shape[1], q.shape[2]
+        lib = _lib.load()
+        _lib.check(lib.bbdg_error_l2(0 if q.dtype == torch.float32 else 1, K, Np, len(self.w), q.data_ptr(),
+                                     d["ET"].data_ptr(), d["w"].data_ptr(), d["lam"].data_ptr(),
+                                     d["verts"].data_ptr(), d["jac"].data_ptr(), float(tau),
+                                     d["partial"].data_ptr(), d["out"].data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream), "bbdg_error_l2")
+        return float(d["out"].item())
 
     def __call__(self, state: FieldState) -> float:
+        if _is_tensor(state.q) and state.q.is_cuda:
+            return self.device(state.q.contiguous(), state.time)
         q0 = state.q[0]
         q0 = q0.double().cpu().numpy() if _is_tensor(q0) else np.asarray(q0, dtype=np.float64)
         ph = q0 @ self.E.T
@@ -474,17 +510,28 @@ def l2_error(system: WaveSystem, state: FieldState, functional: ErrorFunctional 
 
 
 def discrete_energy(system: WaveSystem, state: FieldState) -> float:
-    """sum_k J_k [p^T M p / kappa + rho sum_i u_i^T M u_i] (solver.py:306-312)."""
+    """sum_k J_k [p^T M p / kappa + rho sum_i u_i^T M u_i] (solver.py:306-312).
+
+    Device states: the bbdg_energy kernel (float64 accumulation, deterministic)."""
     M = system.ops_double.mass
     if _is_tensor(state.q):
         torch = _torch()
-        q = state.q.double()
-        Md = torch.as_tensor(np.ascontiguousarray(M), device=q.device)
-        quad = torch.einsum("fkn,nm,fkm->fk", q, Md, q)
-        kap = torch.as_tensor(system.mat.kappa, device=q.device)
-        rho = torch.as_tensor(system.mat.rho, device=q.device)
-        jac = torch.as_tensor(system.mesh.jac, device=q.device)
-        return float(((quad[0] / kap + rho * quad[1:].sum(0)) * jac).sum())
+        q = state.q.contiguous()
+        d = getattr(system, "_energy_dev", None)
+        if d is None or d["M"].device != q.device:
+            f64 = dict(dtype=torch.float64, device=q.device)
+            sl = slice(None) if system._plan is None else slice(system._plan.k0, system._plan.k1)
+            jac = system.mesh.jac[sl]
+            coef = np.stack([jac / system.mat.kappa[sl]] + [jac * system.mat.rho[sl]] * 3)
+            d = dict(M=torch.as_tensor(np.ascontiguousarray(M), **f64),
+                     coef=torch.as_tensor(np.ascontiguousarray(coef), **f64),
+                     partial=torch.empty(q.shape[1], **f64), out=torch.empty(1, **f64))
+            system._energy_dev = d
+        lib = _lib.load()
+        _lib.check(lib.bbdg_energy(0 if q.dtype == torch.float32 else 1, q.shape[1], q.shape[2], q.data_ptr(),
+                                   d["M"].data_ptr(), d["coef"].data_ptr(), d["partial"].data_ptr(),
+                                   d["out"].data_ptr(), torch.cuda.current_stream().cuda_stream), "bbdg_energy")
+        return float(d["out"].item())
     q = np.asarray(state.q, dtype=np.float64)
     quad = np.einsum("fkn,nm,fkm->fk", q, M, q)
     return float(((quad[0] / system.mat.kappa + system.mat.rho * quad[1:].sum(axis=0)) * system.mesh.jac).sum())

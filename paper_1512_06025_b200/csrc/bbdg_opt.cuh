@@ -126,8 +126,9 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // CTA tables (bytes)
   static constexpr int o_tr2 = 0;                                      // u16 [4 f2][6 perm][Nfp] neighbour trace pos
   static constexpr int o_ptab = align16(o_tr2 + 2 * 24 * Nfp);         // u16 [6][Nfp] (halo faces)
-  static constexpr int o_l0c = align16(o_ptab + 2 * 6 * Nfp);          // V4<T> [2][Nfp]
-  static constexpr int o_gfac = align16(o_l0c + 2 * 4 * sz * Nfp);     // V4<T> [Np]
+  static constexpr int o_l0c = align16(o_ptab + 2 * 6 * Nfp);          // V4<T> [Nfp] (d, c0, c1, c2)
+  static constexpr int o_ffac = align16(o_l0c + 4 * sz * Nfp);         // T [Nfp] face-point b!
+  static constexpr int o_gfac = align16(o_ffac + sz * Nfp);            // V4<T> [Np]
   static constexpr int o_l0p = align16(o_gfac + 4 * sz * Np);          // u16 [Nfp][8] L0 lane positions
   static constexpr int tables = align16(o_l0p + 16 * Nfp);
   // stage (units of T; every block 16-byte aligned).  Field stride S = FSR (mod A).
@@ -210,24 +211,17 @@ template <typename T, int N, class L> __device__ void build_opt_tables(unsigned 
         tr2[(f2 * 6 + s2) * Nfp + m] = pos3(N, a[0], a[1], a[2]);
       }
     }
-    // L0 row m scaled by b!: diag 1/2 sum (b_j+1)^2, lane (j,k) 1/2 (b_j+1) b_k (bernstein.py:221-229)
-    const double bf = factorial(b[0]) * factorial(b[1]) * factorial(b[2]);
-    T cv[8];
-    cv[0] = T(bf * 0.5 * double((b[0] + 1) * (b[0] + 1) + (b[1] + 1) * (b[1] + 1) + (b[2] + 1) * (b[2] + 1)));
-    int l = 1;
-    for (int j = 0; j < 3; ++j)
-      for (int k = 0; k < 3; ++k) {
-        if (j == k) continue;
-        cv[l++] = b[k] >= 1 ? T(bf * 0.5 * double((b[j] + 1) * b[k])) : T(0);
-      }
-    cv[7] = T(0);
+    // L0 (bernstein.py:221-229; diag 1/2 sum (b_j+1)^2, lane (j,k) 1/2 (b_j+1) b_k at b+e_j-e_k) in
+    // factorial-scaled variables: with F^[g] = g! F[g], b! (L0 F)[b] = d F^[b] + sum_k c_k sum_{j!=k} F^[b+e_j-e_k],
+    // d = 1/2 sum_j (b_j+1)^2, c_k = 1/2 b_k^2 (zero exactly where the lane b+e_j-e_k does not exist)
+    l0c[m] = V4<T>{T(0.5 * double((b[0] + 1) * (b[0] + 1) + (b[1] + 1) * (b[1] + 1) + (b[2] + 1) * (b[2] + 1))),
+                   T(0.5 * b[0] * b[0]), T(0.5 * b[1] * b[1]), T(0.5 * b[2] * b[2])};
+    reinterpret_cast<T*>(sm + L::o_ffac)[m] = T(factorial(b[0]) * factorial(b[1]) * factorial(b[2]));
     int pp[6];
     l0_lanes<N>(m, pp);
     uint16_t* l0p = reinterpret_cast<uint16_t*>(sm + L::o_l0p) + 8 * m;
     for (int x = 0; x < 6; ++x) l0p[x] = pp[x];
     l0p[6] = l0p[7] = 0;
-    l0c[m] = V4<T>{cv[0], cv[1], cv[2], cv[3]};
-    l0c[Nfp + m] = V4<T>{cv[4], cv[5], cv[6], cv[7]};
   }
 }
 
@@ -258,6 +252,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   const uint16_t* ptab = reinterpret_cast<const uint16_t*>(sm + L::o_ptab);
   const V4<T>* l0c = reinterpret_cast<const V4<T>*>(sm + L::o_l0c);
   const V4<T>* gfac = reinterpret_cast<const V4<T>*>(sm + L::o_gfac);
+  const T* ffac = reinterpret_cast<const T*>(sm + L::o_ffac);
 
   const int tid = threadIdx.x;
   const int g = tid / GT;
@@ -267,7 +262,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   const int lane = tid & 31, wg = ((gtid >> 5) + g) % L::GW;
   const int ltid = wg * 32 + lane;   // logical thread index within the group
   T* gbase = reinterpret_cast<T*>(sm + L::tables + g * L::group_bytes);
-  P2<T>* sflux = reinterpret_cast<P2<T>*>(gbase + L::g_flux);   // [4KE][NFS] (Fp, Fu)
+  T* sflux = gbase + L::g_flux;   // [2][NB]: F^p, F^u (flux times the face point's b!)
   T* sW = gbase + L::g_W;   // [layer j][4KE face][tri(N-j)][p,u], ell- and factorial-scaled
   T* sw = gbase + L::g_w;         // [4][KE][NWS], slot Npm = 0
   auto stage_ptr = [&](int st) { return gbase + st * L::stage_T; };
@@ -512,7 +507,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const T bs = nf.w, ab = fabs(bs);
           const T u = bs * nb[0] - ab * loc[0];   // |Bs| jp
           const T jun = nf.x * (nb[1] - loc[1]) + nf.y * (nb[2] - loc[2]) + nf.z * (nb[3] - loc[3]);
-          sflux[fl] = P2<T>{tp * u - ab * jun, cu * jun - u};
+          const T fb = ffac[s_ef[k] & 0xff];
+          sflux[fl] = fb * (tp * u - ab * jun);
+          sflux[NB + fl] = fb * (cu * jun - u);
         });
       });
       __syncwarp();
@@ -525,7 +522,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         slot<k, 32, NSI>(lane, [&] {
           const int fl = hi16(s_of[k]), m = s_ef[k] & 0xff;
           const int ef = s_ef[k] >> 8;
-          const V4<T> ca = l0c[m], cb = l0c[Nfp + m];
+          const V4<T> c = l0c[m];
           int o0, o1, o2, o3, o4, o5;
           if constexpr (L::HOIST_L0) {
             o0 = lo16(s_l0[k][0]), o1 = hi16(s_l0[k][0]), o2 = lo16(s_l0[k][1]), o3 = hi16(s_l0[k][1]);
@@ -536,10 +533,11 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
             o0 = fb + lo16(lp.x), o1 = fb + hi16(lp.x), o2 = fb + lo16(lp.y), o3 = fb + hi16(lp.y);
             o4 = fb + lo16(lp.z), o5 = fb + hi16(lp.z);
           }
-          const P2<T> f0 = sflux[fl], f1 = sflux[o0], f2 = sflux[o1], f3 = sflux[o2], f4 = sflux[o3],
-                      f5 = sflux[o4], f6 = sflux[o5];
-          const T vp = ca.x * f0.x + ca.y * f1.x + ca.z * f2.x + ca.w * f3.x + cb.x * f4.x + cb.y * f5.x + cb.z * f6.x;
-          const T vu = ca.x * f0.y + ca.y * f1.y + ca.z * f2.y + ca.w * f3.y + cb.x * f4.y + cb.y * f5.y + cb.z * f6.y;
+          // lanes (j,k): 0 (0,1), 1 (0,2), 2 (1,0), 3 (1,2), 4 (2,0), 5 (2,1), grouped by k
+          const T* Fp = sflux;
+          const T* Fu = sflux + NB;
+          const T vp = c.x * Fp[fl] + c.y * (Fp[o2] + Fp[o4]) + c.z * (Fp[o0] + Fp[o5]) + c.w * (Fp[o1] + Fp[o3]);
+          const T vu = c.x * Fu[fl] + c.y * (Fu[o2] + Fu[o4]) + c.z * (Fu[o0] + Fu[o5]) + c.w * (Fu[o1] + Fu[o3]);
           reinterpret_cast<P2<T>*>(sW)[ef * Nfp + m] = P2<T>{vp, vu};   // layer 0
         });
       });

@@ -144,7 +144,10 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // group block (units of T)
   static constexpr int g_flux = 2 * stage_T;                      // [2][NB]
   static constexpr int g_W = rnd(g_flux + (SURF ? 2 * NB : 0));   // [layer j][4KE face][tri(N-j)][p,u]
-  static constexpr int g_w = rnd(g_W + (SURF ? 8 * KE * Np : 0));   // [4][KE][NWS]
+  // V1 output: fp32 4-field vectors V4 [KE][NWS] (one 16-byte load per V2 parent: quarter-warp
+  // conflict domains), fp64 planar [4][KE][NWS] (a 32-byte vector would cost two loads + registers)
+  static constexpr bool WAOS = sz == 4 && N >= 4;   // (measured: planar wins below N = 4)
+  static constexpr int g_w = rnd(g_W + (SURF ? 8 * KE * Np : 0));
   static constexpr int group_T = rnd(g_w + (VOL ? 4 * KE * NWS : 0));
   static constexpr int group_bytes = group_T * sz;
   static constexpr int ng_fit(int budget) {
@@ -264,13 +267,18 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   T* gbase = reinterpret_cast<T*>(sm + L::tables + g * L::group_bytes);
   T* sflux = gbase + L::g_flux;   // [2][NB]: F^p, F^u (flux times the face point's b!)
   T* sW = gbase + L::g_W;   // [layer j][4KE face][tri(N-j)][p,u], ell- and factorial-scaled
-  T* sw = gbase + L::g_w;         // [4][KE][NWS], slot Npm = 0
+  T* swp = gbase + L::g_w;   // V1 output, slot Npm = 0 (see OptLayout::WAOS)
+  V4<T>* sw = reinterpret_cast<V4<T>*>(swp);
   auto stage_ptr = [&](int st) { return gbase + st * L::stage_T; };
   auto stage_bar = [&](int st) { return reinterpret_cast<uint64_t*>(stage_ptr(st) + L::t_bar); };
 
   build_opt_tables<T, N, L>(sm, tid, L::threads);
   if constexpr (L::VOL) {
-    for (int i = gtid; i < 4 * KE; i += GT) sw[i * NWS + Npm] = T(0);   // V2 sentinel slots (never rewritten)
+    if constexpr (L::WAOS) {
+      for (int i = gtid; i < KE; i += GT) sw[i * NWS + Npm] = V4<T>{T(0), T(0), T(0), T(0)};   // V2 sentinels
+    } else {
+      for (int i = gtid; i < 4 * KE; i += GT) swp[i * NWS + Npm] = T(0);
+    }
   }
   if (ltid == 0) {
     mbar_init(stage_bar(0), 1);
@@ -583,14 +591,20 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const T* G = gr + 26;   // rst_dx[m][i] = G[3m+i]
           const T sr = -gr[25] * v1f[k];   // -(1/rho)/2 / beta!
           const T sk = -gr[24] * v1f[k];   // -kappa/2 / beta!
-          T* w = sw + lo16(v1w[k]);
+          T wu[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
-            w[(1 + c) * KE * NWS] = sr * (G[c] * d[0][0] + G[3 + c] * d[0][1] + G[6 + c] * d[0][2]);
+          for (int c = 0; c < 3; ++c) wu[c] = sr * (G[c] * d[0][0] + G[3 + c] * d[0][1] + G[6 + c] * d[0][2]);
           T div = T(0);
 #pragma unroll
           for (int c = 0; c < 3; ++c) div += G[c] * d[1 + c][0] + G[3 + c] * d[1 + c][1] + G[6 + c] * d[1 + c][2];
-          w[0] = sk * div;
+          if constexpr (L::WAOS) {
+            sw[lo16(v1w[k])] = V4<T>{sk * div, wu[0], wu[1], wu[2]};
+          } else {
+            T* w = swp + lo16(v1w[k]);
+            w[0] = sk * div;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) w[(1 + c) * KE * NWS] = wu[c];
+          }
         });
       });
     }
@@ -610,10 +624,18 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         T r[4];
         if constexpr (L::VOL) {
           const int p0 = lo16(v2p[k][0]), p1 = hi16(v2p[k][0]), p2 = lo16(v2p[k][1]), p3 = hi16(v2p[k][1]);
+          if constexpr (L::WAOS) {
+            const V4<T> w0 = sw[p0], w1 = sw[p1], w2 = sw[p2], w3 = sw[p3];
+            r[0] = v2f[k] * ((w0.x + w1.x) + (w2.x + w3.x));
+            r[1] = v2f[k] * ((w0.y + w1.y) + (w2.y + w3.y));
+            r[2] = v2f[k] * ((w0.z + w1.z) + (w2.z + w3.z));
+            r[3] = v2f[k] * ((w0.w + w1.w) + (w2.w + w3.w));
+          } else {
 #pragma unroll
-          for (int F = 0; F < 4; ++F) {
-            const T* w = sw + F * KE * NWS;
-            r[F] = v2f[k] * ((w[p0] + w[p1]) + (w[p2] + w[p3]));
+            for (int F = 0; F < 4; ++F) {
+              const T* w = swp + F * KE * NWS;
+              r[F] = v2f[k] * ((w[p0] + w[p1]) + (w[p2] + w[p3]));
+            }
           }
         }
         if constexpr (L::SURF) {

@@ -84,9 +84,17 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_ke() {
   constexpr int k8[10] = {BBDG_OPT_KE8};
   return SZ == 4 ? k4[N] : k8[N];
 }
-template <int N, int SZ> __host__ __device__ constexpr int opt_max_groups() {
+#ifndef BBDG_OPT_NG_VOL
+#define BBDG_OPT_NG_VOL 8   // volume-only kernels hoist few offsets: more groups for latency hiding
+#endif
+#ifndef BBDG_OPT_NG_SURF
+#define BBDG_OPT_NG_SURF 4
+#endif
+template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_groups() {
   constexpr int g4[10] = {BBDG_OPT_NG4};
   constexpr int g8[10] = {BBDG_OPT_NG8};
+  if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
+  if constexpr (OP == 1) return BBDG_OPT_NG_SURF;  // OP_SURFACE
   return SZ == 4 ? g4[N] : g8[N];
 }
 
@@ -151,7 +159,7 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int group_T = rnd(g_w + (VOL ? 4 * KE * NWS : 0));
   static constexpr int group_bytes = group_T * sz;
   static constexpr int ng_fit(int budget) {
-    for (int n = opt_max_groups<N, sz>(); n >= 1; --n)
+    for (int n = opt_max_groups<N, sz, OP>(); n >= 1; --n)
       if (tables + n * group_bytes <= budget) return n;
     return 0;
   }

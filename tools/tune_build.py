@@ -10,6 +10,7 @@ VARIANTS = {
     "vC": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,4,4,4,4,4,4,4,3,4"],
     "vD": ["-DBBDG_OPT_KE4=0,8,6,4,2,2,1,1,1,1", "-DBBDG_OPT_NG4=0,8,8,8,8,8,8,6,6,5"],
     "vE": ["-DBBDG_OPT_KE4=0,32,24,12,6,6,4,3,2,2", "-DBBDG_OPT_NG4=0,4,4,4,4,4,4,3,3,3"],
+    "vS": ["-DBBDG_OPT_NG_SURF=6"],
     "vF": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,5,5,5,5,5,5,5,3,5"],
     "vG": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,6,6,6,6,6,6,6,4,6"],
 }

@@ -238,21 +238,43 @@ def run_ours(args, rank, world):
                 row["update_ms"], row["update_frac"] = tu, update_bytes(N, s, K) / (tu * 1e-3) / 1e9 / peak
                 row["unfused_gdofs"] = 4 * K * np_of(N) / ((tv + row["surface_optimal_ms"] + tu) * 1e-3) / 1e9
                 del rhs
+            # end to end through the public API with a pinned host state: H2D + 5 stages + D2H
+            # (N > 1: each rank's slab through DistWaveSystem.step_into, max over ranks)
+            host = torch.empty((4, K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
+            host.copy_(q)
+            reps = 2 if args.quick else max(2, min(args.steps, 5))
             if world == 1:
-                # end to end through the public API with a pinned host state: H2D + 5 stages + D2H
-                host = torch.empty((4, K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
-                host.copy_(q)
                 st = FieldState(host.numpy(), "bernstein")
                 lsrk4_step(sy, st, dt, args.lift)   # warm
                 torch.cuda.synchronize()
-                reps = 2 if args.quick else max(2, min(args.steps, 5))
                 t0 = time.perf_counter()
                 for _ in range(reps):
                     lsrk4_step(sy, st, dt, args.lift)
                 torch.cuda.synchronize()
-                row["e2e_ms_step"] = (time.perf_counter() - t0) * 1e3 / reps
-                row["e2e_bytes"] = 2 * host.numel() * host.element_size()
-                del host, st
+                e2e = (time.perf_counter() - t0) * 1e3 / reps
+                del st
+            else:
+                qd, qt, rd = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+
+                def e2e_step():
+                    qd.copy_(host, non_blocking=True)
+                    sy.step_into(qd, qt, rd, dt, args.lift)
+                    host.copy_(qd, non_blocking=True)
+                    torch.cuda.synchronize()
+
+                e2e_step()
+                torch.distributed.barrier()
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    e2e_step()
+                e2e = (time.perf_counter() - t0) * 1e3 / reps
+                tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
+                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+                e2e = float(tt.item())
+                del qd, qt, rd
+            row["e2e_ms_step"] = e2e
+            row["e2e_bytes"] = 2 * host.numel() * host.element_size()
+            del host
             rows[str(N)] = row
             del sy, q, q2, res
             torch.cuda.empty_cache()
@@ -276,16 +298,14 @@ def run_ours(args, rank, world):
                        "traffic": traffic, "kernel": f"opt_kernel<{args.dtype},N={Nd},OP_STAGE> ({args.lift} lift)",
                        "peak_kind": peak_kind, "bytes_per_launch": stage_bytes(Nd, s, K)}
     out["gpu_launches"] = args.steps * len(orders)
-    if world == 1:
-        e2e_ms = sum(r["e2e_ms_step"] for r in rows.values())
-        e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders)
-        out["e2e"] = {"value": e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-                      "h2d_bytes_per_step": sum(r["e2e_bytes"] // 2 for r in rows.values()),
-                      "d2h_bytes_per_step": sum(r["e2e_bytes"] // 2 for r in rows.values()),
-                      "what": "lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"}
-    else:
-        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                      "what": "not measured for N > 1 (the public single-process API is the 1-GPU path)"}
+    e2e_ms = sum(r["e2e_ms_step"] for r in rows.values())
+    e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders)
+    out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+                  "h2d_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
+                  "d2h_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
+                  "what": ("lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"
+                           if world == 1 else "per rank: pinned host slab H2D + DistWaveSystem.step_into (5 "
+                           "exchanged stages) + D2H, max over ranks")}
     if world == 1 and args.nodal and not args.quick:
         out["comparison"] = compare_bases(args, dtype, flush)
     return out, K

@@ -376,7 +376,7 @@ def main():
     ap.add_argument("--n", type=int, default=40, help="cube_mesh(n): K = 6 n^3 per GPU")
     ap.add_argument("--orders", default="1-9")
     ap.add_argument("--lift", default="optimal", choices=["optimal", "factorized", "dense"])
-    ap.add_argument("--cpu-n", type=int, default=8, help="oracle sample mesh cube_mesh(cpu_n)")
+    ap.add_argument("--cpu-n", type=int, default=16, help="oracle sample mesh cube_mesh(cpu_n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodal", dest="nodal", action="store_false", help="skip the nodal NPT comparison")
     ap.add_argument("--quick", action="store_true", help="skip the per-kernel breakdown")

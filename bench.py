@@ -167,15 +167,27 @@ def run_ours(args, rank, world):
     torch.cuda.set_device(dev)
     dtype = np.float32 if args.dtype == "f32" else np.float64
     s = 4 if args.dtype == "f32" else 8
+    mesh_n = {}   # per-order cube size in --fill mode
+
+    def fill_n(N):
+        """cube_mesh(n) whose q, q_out, res + geometry records use args.fill of the device memory."""
+        total = torch.cuda.get_device_properties(dev).total_memory
+        per_elem = 12 * np_of(N) * s + 2 * 36 * s + 20
+        # capped at n = 140 (16.5 M tets): the host-side setup arrays of WaveSystem stay < ~20 GB
+        return min(140, int((args.fill * total / per_elem / 6) ** (1.0 / 3.0)))
+
     if world > 1:
         # weak scaling: a box of world x n^3 cells, one n^3-cell x-slab per rank
         from paper_1512_06025_b200.mesh import box_mesh
 
         mesh = box_mesh(world * args.n, args.n, args.n, lo=(-0.5 * world, -0.5, -0.5), hi=(0.5 * world, 0.5, 0.5))
+    elif args.fill > 0:
+        mesh = None
     else:
         mesh = cube_mesh(args.n)
-    K = mesh.K // world
+    K = mesh.K // world if mesh is not None else 0
     orders = parse_orders(args.orders)
+    Ks = {}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     peak, peak_kind = load_peaks()
 
@@ -196,6 +208,14 @@ def run_ours(args, rank, world):
     gen = torch.Generator(device="cuda").manual_seed(2024 + rank)
     with Clocks(dev) as clk:
         for N in orders:
+            if args.fill > 0:
+                from paper_1512_06025_b200.mesh_device import cube_mesh_device
+
+                mesh_n[N] = fill_n(N)
+                mesh = cube_mesh_device(mesh_n[N])
+                torch.cuda.empty_cache()   # return the builder's scratch before the context allocates
+                K = mesh.K
+            Ks[N] = K
             sy = make_system(N)
             q = torch.randn((4, K, sy.Np), generator=gen, device="cuda", dtype=sy.torch_dtype)
             q2, res = torch.empty_like(q), torch.randn_like(q)
@@ -221,10 +241,10 @@ def run_ours(args, rank, world):
             torch.cuda.synchronize()
             per_n[N] = tot
             t_stage = tot / args.steps
-            ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9
+            ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9   # K of this order's mesh
             row = {"gdofs_stage": 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
                    "stage_gbs": ach, "stage_frac": ach / peak}
-            if not args.quick and world == 1:
+            if not args.quick and world == 1 and args.fill <= 0:
                 rhs = torch.empty_like(q)
                 reps = max(3, args.steps)
                 tv = time_launches(torch, lambda: sy.volume_into(q, rhs), flush, reps)
@@ -240,6 +260,15 @@ def run_ours(args, rank, world):
                 del rhs
             # end to end through the public API with a pinned host state: H2D + 5 stages + D2H
             # (N > 1: each rank's slab through DistWaveSystem.step_into, max over ranks)
+            if args.fill > 0:
+                rows[str(N)] = row
+                row["K"] = K
+                row["hbm_fraction"] = (12 * np_of(N) * s + 2 * 36 * s + 20) * K / torch.cuda.get_device_properties(
+                    dev).total_memory
+                del sy, q, q2, res
+                mesh = None
+                torch.cuda.empty_cache()
+                continue
             host = torch.empty((4, K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
             host.copy_(q)
             reps = 2 if args.quick else max(2, min(args.steps, 5))
@@ -284,20 +313,25 @@ def run_ours(args, rank, world):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
         torch.distributed.barrier()
-    dofs_per_step = sum(4 * K * np_of(N) for N in orders)
+    dofs_per_step = sum(4 * Ks[N] * np_of(N) for N in orders)
     value = world * dofs_per_step * args.steps / (total_ms * 1e-3) / 1e9
     out = dict(per_order=rows, value=value, ms_per_step=total_ms / args.steps, clocks=clk.summary())
     Nd = max(orders, key=lambda N: per_n[N])   # dominant kernel: the order with the largest stage time
     t_d = per_n[Nd] / args.steps
-    ach = stage_bytes(Nd, s, K) / (t_d * 1e-3) / 1e9
+    ach = stage_bytes(Nd, s, Ks[Nd]) / (t_d * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(args.dtype, {}).get(f"n{args.n}", {}).get(str(Nd))
     out["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                        "traffic": traffic, "kernel": f"opt_kernel<{args.dtype},N={Nd},OP_STAGE> ({args.lift} lift)",
-                       "peak_kind": peak_kind, "bytes_per_launch": stage_bytes(Nd, s, K)}
+                       "peak_kind": peak_kind, "bytes_per_launch": stage_bytes(Nd, s, Ks[Nd])}
     out["gpu_launches"] = args.steps * len(orders)
+    if args.fill > 0:
+        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                      "what": "not measured in --fill mode (a host copy of an HBM-filling state does not fit)"}
+        out["fill_meshes"] = {str(N): {"n": mesh_n[N], "K": Ks[N]} for N in orders}
+        return out, Ks[orders[-1]]
     e2e_ms = sum(r["e2e_ms_step"] for r in rows.values())
     e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders)
     out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
@@ -380,6 +414,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodal", dest="nodal", action="store_false", help="skip the nodal NPT comparison")
     ap.add_argument("--quick", action="store_true", help="skip the per-kernel breakdown")
+    ap.add_argument("--fill", type=float, default=0.0,
+                    help="configs[2] HBM-filling sweep: per order a cube_mesh (built on the GPU) whose q, q_out, res "
+                         "use this fraction of device memory (1 GPU; no breakdown / e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -429,6 +466,11 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (standard normal, seed 2024)",
             "config": config, "roofline": out["roofline"], "e2e": out["e2e"], "gpu_launches": out["gpu_launches"],
             "clocks": out["clocks"], "per_order": out["per_order"]}
+    if args.fill > 0:
+        line["config"]["workload"] = (f"BB-DG acoustic LSRK4 stage sweep N={args.orders}, HBM-filling cube meshes "
+                                      f"({args.fill:.2f} of device memory for q, q_out, res), built on the GPU")
+        line["config"]["K"] = {N: v["K"] for N, v in out["fill_meshes"].items()}
+        line["config"]["fill"] = out["fill_meshes"]
     if "comparison" in out:
         line["comparison"] = out["comparison"]
     if not args.no_cpu_baseline:

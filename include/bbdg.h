@@ -119,6 +119,13 @@ int bbdg_error_l2(int dtype, int64_t K, int Np, int nq, const void* q0, const do
                   const double* lam, const double* verts, const double* jac, double tau, double* partial,
                   double* out, void* stream);
 
+/* initial_state (solver.py:264-279) on the device: q (4, K, Np) of the context dtype =
+ * tmat (Np, Np) applied to the standing wave of exact_solution (solver.py:249-261) at the
+ * nodal points lam (Np, 4) (barycentric) of each element (vertices (K, 4, 3)); tmat is
+ * nodal_to_bernstein's matrix for the Bernstein basis and the identity for nodal. */
+int bbdg_project_standing_wave(int dtype, int64_t K, int Np, const double* tmat, const double* lam,
+                               const double* verts, double tau, void* q, void* stream);
+
 /* Introspection used by tests and the benchmark. */
 int bbdg_tile_elems(int N, int dtype);
 int64_t bbdg_kernel_smem(int N, int dtype, int op, int lift, int basis);

@@ -18,6 +18,7 @@ from .solver import (
     discrete_energy,
     exact_solution,
     initial_state,
+    initial_state_device,
     integrate,
     l2_error,
     load_state,

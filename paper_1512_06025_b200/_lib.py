@@ -43,6 +43,7 @@ SIGNATURES = [
     ("bbdg_halo_pack", C.c_int, [_P, _P, _P, _P, _I64, _P]),
     ("bbdg_energy", C.c_int, [C.c_int, _I64, C.c_int, _P, _P, _P, _P, _P, _P]),
     ("bbdg_error_l2", C.c_int, [C.c_int, _I64, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),
+    ("bbdg_project_standing_wave", C.c_int, [C.c_int, _I64, C.c_int, _P, _P, _P, _D, _P, _P]),
     ("bbdg_tile_elems", C.c_int, [C.c_int, C.c_int]),
     ("bbdg_kernel_smem", C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
 ]

@@ -91,6 +91,41 @@ __global__ void __launch_bounds__(kFuncThreads) error_kernel(int64_t K, int Np, 
   if (threadIdx.x == 0) partial[k] = jac[k] * s;
 }
 
+// initial_state (solver.py:264-279) on the device: the standing wave of exact_solution at the
+// element's nodal points x = sum_v lam[a][v] X_v, then coefficients c = Tmat values (Tmat =
+// nodal_to_bernstein's matrix for the Bernstein basis, identity for nodal), float64 arithmetic
+template <typename T>
+__global__ void __launch_bounds__(kFuncThreads) project_kernel(int64_t K, int Np, const double* __restrict__ Tm,
+                                                               const double* __restrict__ lam,
+                                                               const double* __restrict__ verts, double tau,
+                                                               T* __restrict__ q) {
+  extern __shared__ double sv[];   // [4][Np] nodal values
+  const int64_t k = blockIdx.x;
+  const double* X = verts + k * 12;
+  const double pi = 3.14159265358979323846, s3 = 1.7320508075688772;
+  const double ct = cos(s3 * pi * tau), amp = sin(s3 * pi * tau) / s3;
+  for (int a = threadIdx.x; a < Np; a += blockDim.x) {
+    double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) x[d] += lam[a * 4 + v] * X[v * 3 + d];
+    const double cx = cos(pi * x[0]), cy = cos(pi * x[1]), cz = cos(pi * x[2]);
+    const double sx = sin(pi * x[0]), sy = sin(pi * x[1]), sz = sin(pi * x[2]);
+    sv[a] = cx * cy * cz * ct;
+    sv[Np + a] = sx * cy * cz * amp;
+    sv[2 * Np + a] = cx * sy * cz * amp;
+    sv[3 * Np + a] = cx * cy * sz * amp;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * Np; i += blockDim.x) {
+    const int F = i / Np, a = i - F * Np;
+    double c = 0.0;
+    for (int b = 0; b < Np; ++b) c += Tm[(int64_t)a * Np + b] * sv[F * Np + b];
+    q[((int64_t)F * K + k) * Np + a] = (T)c;
+  }
+}
+
 __global__ void __launch_bounds__(kFuncThreads) sum_kernel(int64_t n, const double* __restrict__ partial,
                                                            double* __restrict__ out, int do_sqrt) {
   __shared__ double red[kFuncThreads / 32];
@@ -122,6 +157,15 @@ int error_t(int64_t K, int Np, int nq, const void* q0, const double* ET, const d
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "error kernels");
 }
 
+template <typename T>
+int project_t(int64_t K, int Np, const double* Tm, const double* lam, const double* verts, double tau, void* q,
+              cudaStream_t s) {
+  project_kernel<T><<<(unsigned)K, kFuncThreads, (size_t)4 * Np * sizeof(double), s>>>(K, Np, Tm, lam, verts, tau,
+                                                                                        static_cast<T*>(q));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "projection kernel");
+}
+
 }  // namespace
 }  // namespace bbdg
 
@@ -149,6 +193,16 @@ int bbdg_error_l2(int dtype, int64_t K, int Np, int nq, const void* q0, const do
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == BBDG_F32) return error_t<float>(K, Np, nq, q0, eval_t, wq, lam, verts, jac, ct, partial, out, s);
   if (dtype == BBDG_F64) return error_t<double>(K, Np, nq, q0, eval_t, wq, lam, verts, jac, ct, partial, out, s);
+  return set_error(BBDG_ERR_ARG, "unknown dtype");
+}
+
+int bbdg_project_standing_wave(int dtype, int64_t K, int Np, const double* tmat, const double* lam,
+                               const double* verts, double tau, void* q, void* stream) {
+  if (K < 1 || K >= (int64_t(1) << 31) || Np < 1 || !tmat || !lam || !verts || !q)
+    return set_error(BBDG_ERR_ARG, "bad projection arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == BBDG_F32) return project_t<float>(K, Np, tmat, lam, verts, tau, q, s);
+  if (dtype == BBDG_F64) return project_t<double>(K, Np, tmat, lam, verts, tau, q, s);
   return set_error(BBDG_ERR_ARG, "unknown dtype");
 }
 

@@ -449,6 +449,40 @@ def initial_state(mesh: Mesh, N: int, basis: str, dtype=np.float64, node_kind: s
     return FieldState(q.astype(dtype), basis, tau)
 
 
+def initial_state_device(mesh: Mesh, N: int, basis: str, dtype=np.float64, node_kind: str = "warp_blend",
+                         tau: float = 0.0, chunk: int = 1 << 22) -> FieldState:
+    """initial_state (solver.py:264-279) evaluated on the device by bbdg_project_standing_wave:
+    the state is born in HBM (a CUDA tensor), nothing of size K x Np is formed on the host."""
+    torch = _torch()
+    from .multiindex import barycentric_from_rst
+
+    nops = NodalRefOps.build(N, node_kind)
+    if basis == "bernstein":
+        tm = nops.to_bernstein
+    elif basis == "nodal":
+        tm = np.eye(nops.Np)
+    else:
+        raise ValueError(f"unknown basis {basis!r}")
+    f64 = dict(dtype=torch.float64, device="cuda")
+    tmd = torch.as_tensor(np.array(tm, dtype=np.float64), **f64)
+    lam = torch.as_tensor(np.ascontiguousarray(barycentric_from_rst(nops.nodes)), **f64)
+    tdt = torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
+    K, Np = mesh.K, nops.Np
+    q = torch.empty((4, K, Np), dtype=tdt, device="cuda")
+    lib = _lib.load()
+    tets = mesh.tets
+    for k0 in range(0, K, chunk):
+        k1 = min(K, k0 + chunk)
+        verts = torch.as_tensor(np.ascontiguousarray(mesh.vertices[tets[k0:k1]]), **f64)
+        part = torch.empty((4, k1 - k0, Np), dtype=tdt, device="cuda")
+        _lib.check(lib.bbdg_project_standing_wave(0 if tdt == torch.float32 else 1, k1 - k0, Np, tmd.data_ptr(),
+                                                  lam.data_ptr(), verts.data_ptr(), float(tau), part.data_ptr(),
+                                                  torch.cuda.current_stream().cuda_stream),
+                   "bbdg_project_standing_wave")
+        q[:, k0:k1] = part
+    return FieldState(q, basis, tau)
+
+
 class ErrorFunctional:
     """Quadrature of (p_h - p)^2 with a degree 2N+2 rule (solver.py:282-296).
 
@@ -523,7 +557,7 @@ def discrete_energy(system: WaveSystem, state: FieldState) -> float:
             sl = slice(None) if system._plan is None else slice(system._plan.k0, system._plan.k1)
             jac = system.mesh.jac[sl]
             coef = np.stack([jac / system.mat.kappa[sl]] + [jac * system.mat.rho[sl]] * 3)
-            d = dict(M=torch.as_tensor(np.ascontiguousarray(M), **f64),
+            d = dict(M=torch.as_tensor(np.array(M, dtype=np.float64), **f64),
                      coef=torch.as_tensor(np.ascontiguousarray(coef), **f64),
                      partial=torch.empty(q.shape[1], **f64), out=torch.empty(1, **f64))
             system._energy_dev = d

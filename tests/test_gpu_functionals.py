@@ -10,7 +10,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from conftest import rel_l2  # noqa: F401
+from conftest import rel_l2
 from paper_1512_06025_b200 import (BernsteinRefOps, ErrorFunctional, FieldState, Materials, NodalRefOps, WaveSystem,
                                    cube_mesh, discrete_energy, initial_state, integrate, stable_dt)
 
@@ -105,3 +105,18 @@ def test_roundoff_band_criterion_8(sens):
         assert len(ref) == len(traj[basis])
         assert np.all(traj[basis] <= 2 * ref) and np.all(ref <= 2 * traj[basis]), basis
     assert (traj["bernstein"] / traj["nodal"]).max() <= 2.0
+
+
+@pytest.mark.parametrize("basis", ["bernstein", "nodal"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_initial_state_device_matches_host(basis, dtype):
+    from paper_1512_06025_b200 import initial_state_device
+
+    m = cube_mesh(3)
+    for N in (1, 4, 9):
+        host = initial_state(m, N, basis, dtype=dtype, tau=0.37)
+        dev = initial_state_device(m, N, basis, dtype=dtype, tau=0.37, chunk=50)   # several chunks
+        got = dev.q.cpu().numpy()
+        assert got.dtype == dtype and dev.time == 0.37
+        tol = 1e-13 if dtype == np.float64 else 1e-6
+        assert rel_l2(got, host.q) < tol, (N, rel_l2(got, host.q))

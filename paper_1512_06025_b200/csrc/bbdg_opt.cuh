@@ -90,11 +90,18 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_ke() {
 #ifndef BBDG_OPT_NG_SURF
 #define BBDG_OPT_NG_SURF 4
 #endif
+#ifndef BBDG_OPT_TMEM
+#define BBDG_OPT_TMEM 1
+#endif
+#ifndef BBDG_OPT_NG_TMEM
+#define BBDG_OPT_NG_TMEM 5   // groups of the fused fp32 kernels whose hoisted tables live in TMEM
+#endif
 template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_groups() {
   constexpr int g4[10] = {BBDG_OPT_NG4};
   constexpr int g8[10] = {BBDG_OPT_NG8};
   if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
   if constexpr (OP == 1) return BBDG_OPT_NG_SURF;  // OP_SURFACE
+  if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= 5) return BBDG_OPT_NG_TMEM;
   return SZ == 4 ? g4[N] : g8[N];
 }
 
@@ -164,6 +171,20 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
     return 0;
   }
   static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
+  // hoisted per-thread tables parked in TMEM (fused fp32 kernels at high order, where
+  // registers cap the group count): flat 32-bit word offsets of each table
+  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= 5;
+  static constexpr int SSa_ = SS > 0 ? SS : 1, SV1a_ = SV1 > 0 ? SV1 : 1;
+  static constexpr int C3W = (S3T + 1) / 2 > 0 ? (S3T + 1) / 2 : 1;
+  static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);
+  static constexpr int H_V1C = H_C3 + C3W, H_V1W = H_V1C + 2 * SV1a_, H_V1F = H_V1W + SV1a_;
+  static constexpr int H_V2P = H_V1F + SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
+  static constexpr int H_V2F = H_V2M + SV2, NH = H_V2F + SV2;
+  static constexpr int tm_cols() {
+    int c = 32;
+    while (c < NG * NH) c *= 2;
+    return c;
+  }
   static constexpr int threads = NG * GT;
   static constexpr int total = tables + NG * group_bytes;
   static_assert(4 * KE * NPS < 65536 && KE * Np < 65536, "u16 offsets");
@@ -235,6 +256,58 @@ template <typename T, int N, class L> __device__ void build_opt_tables(unsigned 
     l0p[6] = l0p[7] = 0;
   }
 }
+
+// ----------------------------------------------------------------------------
+// TMEM as a per-lane store for the hoisted per-thread tables (tcgen05.ld/st, 32x32b shape:
+// thread t of warp w owns TMEM lane 32 (w % 4) + t).  The tables are written once after the
+// prologue and re-read phase by phase, so they do not occupy registers across the tile loop.
+// ----------------------------------------------------------------------------
+template <int C> __device__ __forceinline__ void tm_st(uint32_t ta, const uint32_t* r) {
+  if constexpr (C >= 16) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+                 ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+                 : "memory");
+    tm_st<C - 16>(ta + 16, r + 16);
+  } else if constexpr (C >= 8) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(ta), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+    tm_st<C - 8>(ta + 8, r + 8);
+  } else if constexpr (C >= 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+    tm_st<C - 4>(ta + 4, r + 4);
+  } else if constexpr (C >= 2) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]) : "memory");
+    tm_st<C - 2>(ta + 2, r + 2);
+  } else if constexpr (C == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(ta), "r"(r[0]) : "memory");
+  }
+}
+template <int C> __device__ __forceinline__ void tm_ld(uint32_t ta, uint32_t* r) {
+  if constexpr (C >= 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta)
+                 : "memory");
+    tm_ld<C - 8>(ta + 8, r + 8);
+  } else if constexpr (C >= 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(ta)
+                 : "memory");
+    tm_ld<C - 4>(ta + 4, r + 4);
+  } else if constexpr (C >= 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(ta) : "memory");
+    tm_ld<C - 2>(ta + 2, r + 2);
+  } else if constexpr (C == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r[0]) : "r"(ta) : "memory");
+  }
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t lo16(uint32_t x) { return x & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t x) { return x >> 16; }
@@ -385,6 +458,111 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     v2f[k] = T(factorial(al[0]) * factorial(al[1]) * factorial(al[2]) * factorial(al[3]));
   }
 
+  // ---------------------------------------------------------------- park the tables in TMEM
+  __shared__ uint32_t tm_slot;
+  uint32_t ta = 0;
+  if constexpr (L::TMH) {
+    const int pw_id = tid >> 5;
+    if (pw_id == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tm_slot)),
+                   "n"(L::tm_cols()));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    ta = tm_slot + ((uint32_t)(32 * (pw_id & 3)) << 16) + (uint32_t)((pw_id >> 2) * L::NH);
+    uint32_t hx[L::NH];
+#pragma unroll
+    for (int x = 0; x < L::NH; ++x) hx[x] = 0;
+#pragma unroll
+    for (int k = 0; k < SS; ++k) {
+      hx[L::H_SOF + k] = s_of[k];
+      hx[L::H_SEF + k] = s_ef[k];
+      if constexpr (L::HOIST_L0) {
+        hx[L::H_SL0 + 3 * k] = s_l0[k][0];
+        hx[L::H_SL0 + 3 * k + 1] = s_l0[k][1];
+        hx[L::H_SL0 + 3 * k + 2] = s_l0[k][2];
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < L::C3W; ++x) hx[L::H_C3 + x] = c3[x];
+#pragma unroll
+    for (int k = 0; k < SV1; ++k) {
+      hx[L::H_V1C + 2 * k] = v1c[k][0];
+      hx[L::H_V1C + 2 * k + 1] = v1c[k][1];
+      hx[L::H_V1W + k] = v1w[k];
+      hx[L::H_V1F + k] = __float_as_uint((float)v1f[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < SV2; ++k) {
+      hx[L::H_V2P + 2 * k] = v2p[k][0];
+      hx[L::H_V2P + 2 * k + 1] = v2p[k][1];
+      hx[L::H_V2G + 2 * k] = v2g[k][0];
+      hx[L::H_V2G + 2 * k + 1] = v2g[k][1];
+      hx[L::H_V2M + k] = v2m[k];
+      hx[L::H_V2F + k] = __float_as_uint((float)v2f[k]);
+    }
+    tm_st<L::NH>(ta, hx);
+    tm_wait_st();
+  }
+  // reload one phase's tables from TMEM (no-op when they stay in registers)
+  auto tm_load_s = [&] {
+    if constexpr (L::TMH) {
+      uint32_t t[2 * SSa];
+      tm_ld<2 * SSa>(ta + L::H_SOF, t);
+      uint32_t u[3 * SSa];
+      if constexpr (L::HOIST_L0) tm_ld<3 * SSa>(ta + L::H_SL0, u);
+      tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SS; ++k) {
+        s_of[k] = t[k];
+        s_ef[k] = t[SSa + k];
+        if constexpr (L::HOIST_L0) {
+          s_l0[k][0] = u[3 * k];
+          s_l0[k][1] = u[3 * k + 1];
+          s_l0[k][2] = u[3 * k + 2];
+        }
+      }
+    }
+  };
+  auto tm_load_c3 = [&] {
+    if constexpr (L::TMH) {
+      tm_ld<L::C3W>(ta + L::H_C3, c3);
+      tm_wait_ld();
+    }
+  };
+  auto tm_load_v1 = [&] {
+    if constexpr (L::TMH) {
+      uint32_t t[4 * SV1a];
+      tm_ld<4 * SV1a>(ta + L::H_V1C, t);
+      tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SV1; ++k) {
+        v1c[k][0] = t[2 * k];
+        v1c[k][1] = t[2 * k + 1];
+        v1w[k] = t[2 * SV1a + k];
+        v1f[k] = (T)__uint_as_float(t[3 * SV1a + k]);
+      }
+    }
+  };
+  auto tm_load_v2 = [&] {
+    if constexpr (L::TMH) {
+      uint32_t t[6 * SV2];
+      tm_ld<6 * SV2>(ta + L::H_V2P, t);
+      tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SV2; ++k) {
+        v2p[k][0] = t[2 * k];
+        v2p[k][1] = t[2 * k + 1];
+        v2g[k][0] = t[2 * SV2 + 2 * k];
+        v2g[k][1] = t[2 * SV2 + 2 * k + 1];
+        v2m[k] = t[4 * SV2 + k];
+        v2f[k] = (T)__uint_as_float(t[5 * SV2 + k]);
+      }
+    }
+  };
+
   // ---------------------------------------------------------------- staging
   const int64_t fs = p.K * Np;
   const T* __restrict__ q = p.q;
@@ -491,6 +669,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     const bool has_next = tn < ntiles;
     const int64_t k0n = has_next ? tile_k0(tn) : 0;
     const int nvn = has_next ? tile_nv(tn) : 0;
+    tm_load_s();
     if (has_next) {
       if (wg == L::GW - 1) {
         fence_proxy_async();
@@ -558,6 +737,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         });
       });
       // ------------------------------------------------------------- S3: reduction cascade (Alg. 1)
+      tm_load_c3();
       static_for<1, N + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
@@ -580,6 +760,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
 
     // ------------------------------------------------------------- V1: volume, degree N-1 half
     if constexpr (L::VOL) {
+      tm_load_v1();
       static_for<0, SV1>([&](auto KK) {
         constexpr int k = decltype(KK)::value;
         slot<k, GT, KE * Npm>(ltid, [&] {
@@ -619,6 +800,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     group_sync<GT>(g);
 
     // ------------------------------------------------------------- V2 + lift gather + epilogue
+    tm_load_v2();
     T* outF = p.out + k0 * Np;
     T* resF = p.res + k0 * Np;
     static_for<0, SV2>([&](auto KK) {
@@ -698,6 +880,12 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     });
     cp_async_wait_all();
     group_sync<GT>(g);   // neighbour traces landed; this stage / work buffers free
+  }
+  if constexpr (L::TMH) {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if ((tid >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tm_slot), "n"(L::tm_cols()));
   }
 }
 

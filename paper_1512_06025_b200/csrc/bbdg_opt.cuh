@@ -96,12 +96,15 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_ke() {
 #ifndef BBDG_OPT_NG_TMEM
 #define BBDG_OPT_NG_TMEM 5   // groups of the fused fp32 kernels whose hoisted tables live in TMEM
 #endif
+#ifndef BBDG_OPT_TMEM_MIN_N
+#define BBDG_OPT_TMEM_MIN_N 4   // (measured: no gain below N = 4, where registers do not bind)
+#endif
 template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_groups() {
   constexpr int g4[10] = {BBDG_OPT_NG4};
   constexpr int g8[10] = {BBDG_OPT_NG8};
   if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
   if constexpr (OP == 1) return BBDG_OPT_NG_SURF;  // OP_SURFACE
-  if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= 5) return BBDG_OPT_NG_TMEM;
+  if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
   return SZ == 4 ? g4[N] : g8[N];
 }
 
@@ -173,7 +176,7 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
   // hoisted per-thread tables parked in TMEM (fused fp32 kernels at high order, where
   // registers cap the group count): flat 32-bit word offsets of each table
-  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= 5;
+  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= BBDG_OPT_TMEM_MIN_N;
   static constexpr int SSa_ = SS > 0 ? SS : 1, SV1a_ = SV1 > 0 ? SV1 : 1;
   static constexpr int C3W = (S3T + 1) / 2 > 0 ? (S3T + 1) / 2 : 1;
   static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);

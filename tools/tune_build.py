@@ -7,6 +7,8 @@ from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
 F64 = {"vH", "vI"}
 VARIANTS = {
+    "vJ": ["-DBBDG_OPT_NG_TMEM=6"],
+    "vK": ["-DBBDG_OPT_NG_TMEM=6", "-DBBDG_OPT_TMEM_MIN_N=2"],
     "vH": ["-DBBDG_OPT_KE8=0,16,12,6,4,3,2,2,1,1"],
     "vI": ["-DBBDG_OPT_KE8=0,32,24,12,6,4,3,2,2,1"],
     "vB": ["-DBBDG_OPT_KE4=0,16,12,6,4,2,2,1,1,1", "-DBBDG_OPT_NG4=0,8,8,8,6,6,6,4,4,4"],

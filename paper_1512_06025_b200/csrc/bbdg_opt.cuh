@@ -182,7 +182,9 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);
   static constexpr int H_V1C = H_C3 + C3W, H_V1W = H_V1C + 2 * SV1a_, H_V1F = H_V1W + SV1a_;
   static constexpr int H_V2P = H_V1F + SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
-  static constexpr int H_V2F = H_V2M + SV2, NH = H_V2F + SV2;
+  static constexpr int H_V2F = H_V2M + SV2;
+  // per-point coefficients (TMEM mode only): L0 4-vector + b! per S slot, gather 1/beta! 4-vector per V2 slot
+  static constexpr int H_L0C = H_V2F + SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_, NH = H_GF + 4 * SV2;
   static constexpr int tm_cols() {
     int c = 32;
     while (c < NG * NH) c *= 2;
@@ -506,9 +508,30 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_V2M + k] = v2m[k];
       hx[L::H_V2F + k] = __float_as_uint((float)v2f[k]);
     }
+#pragma unroll
+    for (int k = 0; k < SS; ++k) {
+      const int m = s_ef[k] & 0xff;
+      const V4<T> c = l0c[m];
+      hx[L::H_L0C + 4 * k] = __float_as_uint((float)c.x);
+      hx[L::H_L0C + 4 * k + 1] = __float_as_uint((float)c.y);
+      hx[L::H_L0C + 4 * k + 2] = __float_as_uint((float)c.z);
+      hx[L::H_L0C + 4 * k + 3] = __float_as_uint((float)c.w);
+      hx[L::H_FF + k] = __float_as_uint((float)ffac[m]);
+    }
+#pragma unroll
+    for (int k = 0; k < SV2; ++k) {
+      const V4<T> gf = gfac[hi16(v2m[k]) & 1023];
+      hx[L::H_GF + 4 * k] = __float_as_uint((float)gf.x);
+      hx[L::H_GF + 4 * k + 1] = __float_as_uint((float)gf.y);
+      hx[L::H_GF + 4 * k + 2] = __float_as_uint((float)gf.z);
+      hx[L::H_GF + 4 * k + 3] = __float_as_uint((float)gf.w);
+    }
     tm_st<L::NH>(ta, hx);
     tm_wait_st();
   }
+  // per-point coefficients, from TMEM in TMEM mode (filled by the phase loads below)
+  V4<T> tl0[L::TMH ? SSa : 1], tgf[L::TMH ? SV2 : 1];
+  T tff[L::TMH ? SSa : 1];
   // reload one phase's tables from TMEM (no-op when they stay in registers)
   auto tm_load_s = [&] {
     if constexpr (L::TMH) {
@@ -516,7 +539,15 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       tm_ld<2 * SSa>(ta + L::H_SOF, t);
       uint32_t u[3 * SSa];
       if constexpr (L::HOIST_L0) tm_ld<3 * SSa>(ta + L::H_SL0, u);
+      uint32_t cf[5 * SSa];
+      tm_ld<5 * SSa>(ta + L::H_L0C, cf);
       tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SS; ++k) {
+        tl0[k] = V4<T>{(T)__uint_as_float(cf[4 * k]), (T)__uint_as_float(cf[4 * k + 1]),
+                       (T)__uint_as_float(cf[4 * k + 2]), (T)__uint_as_float(cf[4 * k + 3])};
+        tff[k] = (T)__uint_as_float(cf[4 * SSa + k]);
+      }
 #pragma unroll
       for (int k = 0; k < SS; ++k) {
         s_of[k] = t[k];
@@ -553,7 +584,13 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     if constexpr (L::TMH) {
       uint32_t t[6 * SV2];
       tm_ld<6 * SV2>(ta + L::H_V2P, t);
+      uint32_t gq[4 * SV2];
+      tm_ld<4 * SV2>(ta + L::H_GF, gq);
       tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SV2; ++k)
+        tgf[k] = V4<T>{(T)__uint_as_float(gq[4 * k]), (T)__uint_as_float(gq[4 * k + 1]),
+                       (T)__uint_as_float(gq[4 * k + 2]), (T)__uint_as_float(gq[4 * k + 3])};
 #pragma unroll
       for (int k = 0; k < SV2; ++k) {
         v2p[k][0] = t[2 * k];
@@ -705,7 +742,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const T bs = nf.w, ab = fabs(bs);
           const T u = bs * nb[0] - ab * loc[0];   // |Bs| jp
           const T jun = nf.x * (nb[1] - loc[1]) + nf.y * (nb[2] - loc[2]) + nf.z * (nb[3] - loc[3]);
-          const T fb = ffac[s_ef[k] & 0xff];
+          T fb;
+          if constexpr (L::TMH) fb = tff[k];
+          else fb = ffac[s_ef[k] & 0xff];
           sflux[fl] = fb * (tp * u - ab * jun);
           sflux[NB + fl] = fb * (cu * jun - u);
         });
@@ -720,7 +759,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         slot<k, 32, NSI>(lane, [&] {
           const int fl = hi16(s_of[k]), m = s_ef[k] & 0xff;
           const int ef = s_ef[k] >> 8;
-          const V4<T> c = l0c[m];
+          V4<T> c;
+          if constexpr (L::TMH) c = tl0[k];
+          else c = l0c[m];
           int o0, o1, o2, o3, o4, o5;
           if constexpr (L::HOIST_L0) {
             o0 = lo16(s_l0[k][0]), o1 = hi16(s_l0[k][0]), o2 = lo16(s_l0[k][1]), o3 = hi16(s_l0[k][1]);
@@ -833,7 +874,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         }
         if constexpr (L::SURF) {
           const int g0 = lo16(v2g[k][0]), g1 = hi16(v2g[k][0]), g2 = lo16(v2g[k][1]), g3 = hi16(v2g[k][1]);
-          const V4<T> gf = gfac[a];
+          V4<T> gf;
+          if constexpr (L::TMH) gf = tgf[k];
+          else gf = gfac[a];
           const P2<T>* W2 = reinterpret_cast<const P2<T>*>(sW);
           const P2<T> w0 = W2[g0], w1 = W2[g1], w2 = W2[g2], w3 = W2[g3];
           const T sp = gf.x * w0.x + gf.y * w1.x + gf.z * w2.x + gf.w * w3.x;

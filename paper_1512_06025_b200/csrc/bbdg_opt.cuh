@@ -125,7 +125,9 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // slot counts (items per thread, rounded up); a slot is "full" if every thread has an item
   static constexpr int NS_ITEMS = PPW * Nfp;
   static constexpr int SS = SURF ? (NS_ITEMS + 31) / 32 : 0;
-  static constexpr bool HOIST_L0 = SS <= 2;   // L0 lane offsets in registers (else one LDS.128 per item)
+  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= BBDG_OPT_TMEM_MIN_N;
+  // L0 lane offsets hoisted (registers, or TMEM in TMEM mode) -- else one LDS.128 per item
+  static constexpr bool HOIST_L0 = SS <= 2 || TMH;
   static constexpr int SV1 = VOL ? (KE * Npm + GT - 1) / GT : 0;
   static constexpr int SV2 = (KE * Np + GT - 1) / GT;
   // cascade items are single-field: 2 PPW face-fields x tri_dim(N-j) per warp at level j
@@ -176,7 +178,6 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
   // hoisted per-thread tables parked in TMEM (fused fp32 kernels at high order, where
   // registers cap the group count): flat 32-bit word offsets of each table
-  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= BBDG_OPT_TMEM_MIN_N;
   static constexpr int SSa_ = SS > 0 ? SS : 1, SV1a_ = SV1 > 0 ? SV1 : 1;
   static constexpr int C3W = (S3T + 1) / 2 > 0 ? (S3T + 1) / 2 : 1;
   static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);

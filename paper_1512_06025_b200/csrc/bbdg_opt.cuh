@@ -185,7 +185,9 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int H_V2P = H_V1F + SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
   static constexpr int H_V2F = H_V2M + SV2;
   // per-point coefficients (TMEM mode only): L0 4-vector + b! per S slot, gather 1/beta! 4-vector per V2 slot
-  static constexpr int H_L0C = H_V2F + SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_, NH = H_GF + 4 * SV2;
+  static constexpr int H_L0C = H_V2F + SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_;
+  // cascade items with resolved smem byte offsets (rel. the dynamic smem base) of their children
+  static constexpr int H_C3B = H_GF + 4 * SV2, NH = H_C3B + 2 * (S3T > 0 ? S3T : 1);
   static constexpr int tm_cols() {
     int c = 32;
     while (c < NG * NH) c *= 2;
@@ -527,6 +529,22 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_GF + 4 * k + 2] = __float_as_uint((float)gf.z);
       hx[L::H_GF + 4 * k + 3] = __float_as_uint((float)gf.w);
     }
+    if constexpr (L::SURF) {
+      static_for<1, N + 1>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        constexpr int ml = N - j, nhi = tri_dim(ml + 1);
+        const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
+#pragma unroll
+        for (int k = 0; k < L::s3_slots(j); ++k) {
+          const int x = L::s3_base(j) + k;
+          const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+          const T* rd = Br + 32 * k + (c & 0xff);
+          const T* r3 = rd - ((c >> 8) & 0xff) + 2 * (ml + 2);
+          hx[L::H_C3B + 2 * x] = (uint32_t)(reinterpret_cast<const unsigned char*>(rd) - sm);
+          hx[L::H_C3B + 2 * x + 1] = (uint32_t)(reinterpret_cast<const unsigned char*>(r3) - sm);
+        }
+      });
+    }
     tm_st<L::NH>(ta, hx);
     tm_wait_st();
   }
@@ -561,12 +579,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       }
     }
   };
-  auto tm_load_c3 = [&] {
-    if constexpr (L::TMH) {
-      tm_ld<L::C3W>(ta + L::H_C3, c3);
-      tm_wait_ld();
-    }
-  };
+  auto tm_load_c3 = [&] {};   // TMEM mode: the cascade reads resolved offsets per level
   auto tm_load_v1 = [&] {
     if constexpr (L::TMH) {
       uint32_t t[4 * SV1a];
@@ -786,18 +799,29 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       static_for<1, N + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
+        constexpr int NSL = L::s3_slots(j);
         const T kap = T(cascade_kappa(N, j));
         T* const Bw = sW + 8 * KE * layer_off(N, j) + 2 * wg * PPW * nlo + lane;
         const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
+        uint32_t cb[L::TMH ? 2 * NSL : 1];
+        if constexpr (L::TMH) tm_ld<2 * NSL>(ta + L::H_C3B + 2 * L::s3_base(j), cb);
         __syncwarp();
-        static_for<0, L::s3_slots(j)>([&](auto KK) {
+        if constexpr (L::TMH) tm_wait_ld();
+        static_for<0, NSL>([&](auto KK) {
           constexpr int k = decltype(KK)::value;
           constexpr int x = L::s3_base(j) + k;
           slot<k, 32, L::s3_items(j)>(lane, [&] {
-            const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
-            const T* rd = Br + 32 * k + (c & 0xff);
-            const T* r3 = rd - ((c >> 8) & 0xff);
-            Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
+            if constexpr (L::TMH) {
+              // children at resolved smem byte offsets: e2 / e1 (pair-adjacent) and e0
+              const T* rd = reinterpret_cast<const T*>(sm + cb[2 * k]);
+              const T* r3 = reinterpret_cast<const T*>(sm + cb[2 * k + 1]);
+              Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[0]);
+            } else {
+              const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+              const T* rd = Br + 32 * k + (c & 0xff);
+              const T* r3 = rd - ((c >> 8) & 0xff);
+              Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
+            }
           });
         });
       });

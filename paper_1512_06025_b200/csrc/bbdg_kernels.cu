@@ -66,7 +66,7 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal)");
     attr = true;
   }
-  const int64_t ntiles = (nl + NodalMma<T>::MT - 1) / NodalMma<T>::MT;
+  const int64_t ntiles = (nl + L::ET - 1) / L::ET;
   kern<<<(unsigned)std::min<int64_t>(ntiles, num_sms), L::THREADS, L::total, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal MMA kernel launch");

@@ -38,7 +38,7 @@ template <> struct NodalMma<float> {
     return r;
   }
   __device__ static void mma(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
                  "{%0,%1,%2,%3};\n"
                  : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -75,13 +75,20 @@ template <> struct NodalMma<double> {
   }
   __device__ static void step(double* c, const double* a, const double* alo, const BFrag& b) {
     (void)alo;
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a[0]), "d"(b));
   }
   __device__ static int crow(int g, int i) { return g; }
   __device__ static int ccol(int t, int i) { return 2 * t + i; }
 };
+
+// 4/8-byte cp.async with zero fill (src-size 0) for padding
+template <typename T> __device__ __forceinline__ void stage_cp(uint32_t dst, const T* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(src), "n"(sizeof(T)),
+               "r"(ok ? (int)sizeof(T) : 0)
+               : "memory");
+}
 
 template <typename T, int N> struct NodalLayout {
   using M = NodalMma<T>;
@@ -100,8 +107,12 @@ template <typename T, int N> struct NodalLayout {
   }
   static constexpr int LQ = pitch(KQ * M::KS), LF = pitch(KF * M::KS);
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
-  static constexpr int sq = 0, sf = 4 * M::MT * LQ;           // [4][MT][LQ], [4][MT][LF]
-  static constexpr int total = (sf + 4 * M::MT * LF) * (int)sizeof(T);
+  // element M-tiles per CTA: enough that every warp has an (M-tile, n-tile) pair at low order
+  static constexpr int R = NTL >= WARPS ? 1 : WARPS / NTL;
+  static constexpr int WPM = WARPS / R;                        // warps per M-tile
+  static constexpr int ET = R * M::MT;                         // elements per CTA tile
+  static constexpr int sq = 0, sf = 4 * ET * LQ;               // [4][ET][LQ], [4][ET][LF]
+  static constexpr int total = (sf + 4 * ET * LF) * (int)sizeof(T);
 };
 
 // Face fluxes of the nodal path, one thread per (element, face, point):
@@ -176,40 +187,51 @@ __global__ void __launch_bounds__(NodalLayout<T, N>::THREADS, 1) nodal_mma_kerne
   T* sf = reinterpret_cast<T*>(smraw) + L::sf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int64_t fs = p.K * Np, nl = p.kend - p.kbeg;
-  const int64_t ntiles = (nl + MT - 1) / MT;
+  const int64_t ntiles = (nl + L::ET - 1) / L::ET;
   const auto* bvol = static_cast<const typename M::BFrag*>(p.bvol);
   const auto* blift = static_cast<const typename M::BFrag*>(p.blift);
 
+  constexpr int ET = L::ET;
+  const int mr = warp / L::WPM;          // this warp's M-tile within the CTA tile
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t k0 = p.kbeg + tile * MT;
-    const int nv = (int)((p.kend - k0) < MT ? (p.kend - k0) : MT);
-    // stage the tile (zero padding beyond Np / 4 Nfp and beyond the last element)
+    const int64_t kt = p.kbeg + tile * ET;
+    const int nvt = (int)((p.kend - kt) < ET ? (p.kend - kt) : ET);
+    // stage the tile with cp.async (non-blocking; zero fill beyond Np / 4 Nfp and the last element)
     if constexpr (VOL) {
-      for (int i = tid; i < 4 * MT * LQ; i += L::THREADS) {
-        const int F = i / (MT * LQ), r = i - F * MT * LQ, e = r / LQ, c = r - e * LQ;
-        sq[i] = (e < nv && c < Np) ? p.q[F * fs + (k0 + e) * Np + c] : T(0);
+      const uint32_t sb = smem_u32(sq);
+      for (int i = tid; i < 4 * ET * LQ; i += L::THREADS) {
+        const int F = i / (ET * LQ), r = i - F * ET * LQ, e = r / LQ, c = r - e * LQ;
+        const bool ok = e < nvt && c < Np;
+        stage_cp<T>(sb + i * (int)sizeof(T), ok ? p.q + F * fs + (kt + e) * Np + c : p.q, ok);
       }
     }
     if constexpr (SURF) {
-      for (int i = tid; i < 4 * MT * LF; i += L::THREADS) {
-        const int F = i / (MT * LF), r = i - F * MT * LF, e = r / LF, c = r - e * LF;
-        sf[i] = (e < nv && c < 4 * Nfp) ? p.flux[(F * nl + (k0 - p.kbeg + e)) * 4 * Nfp + c] : T(0);
+      const uint32_t sb = smem_u32(sf);
+      for (int i = tid; i < 4 * ET * LF; i += L::THREADS) {
+        const int F = i / (ET * LF), r = i - F * ET * LF, e = r / LF, c = r - e * LF;
+        const bool ok = e < nvt && c < 4 * Nfp;
+        stage_cp<T>(sb + i * (int)sizeof(T), ok ? p.flux + (F * nl + (kt - p.kbeg + e)) * 4 * Nfp + c : p.flux, ok);
       }
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
+    const int64_t k0 = kt + mr * MT;
+    const int nv = (int)(nvt - mr * MT < 0 ? 0 : (nvt - mr * MT < MT ? nvt - mr * MT : MT));
+    const T* sqm = sq + mr * MT * LQ;    // this M-tile's rows (field stride ET LQ)
+    const T* sfm = sf + mr * MT * LF;
     // geometry of this lane's accumulator rows (elements)
     T G[2][9], kap[2], irho[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int e = M::crow(g, 2 * h);
-      const int64_t k = k0 + (e < nv ? e : 0);
+      const int64_t k = e < nv ? k0 + e : kt;
       const T* gv = p.geo_vol + k * kGeoVol;
 #pragma unroll
       for (int j = 0; j < 9; ++j) G[h][j] = gv[j];
       kap[h] = gv[9];
       irho[h] = gv[10];
     }
-    for (int nt = warp; nt < NTL; nt += L::WARPS) {
+    for (int nt = warp % L::WPM; nt < NTL && nv > 0; nt += L::WPM) {
       T acc[3][4][M::CR], accl[4][M::CR];
 #pragma unroll
       for (int i = 0; i < M::CR; ++i) {
@@ -225,7 +247,7 @@ __global__ void __launch_bounds__(NodalLayout<T, N>::THREADS, 1) nodal_mma_kerne
         for (int ks = 0; ks < KQ; ++ks) {
           AT ah[4][M::AR], al[4][M::AR];
 #pragma unroll
-          for (int F = 0; F < 4; ++F) M::load_a(sq + F * MT * LQ + ks * KS, LQ, g, t, ah[F], al[F]);
+          for (int F = 0; F < 4; ++F) M::load_a(sqm + F * ET * LQ + ks * KS, LQ, g, t, ah[F], al[F]);
 #pragma unroll
           for (int m = 0; m < 3; ++m) {
             const typename M::BFrag b = __ldg(bvol + (((int64_t)m * KQ + ks) * NTL + nt) * 32 + lane);
@@ -241,7 +263,7 @@ __global__ void __launch_bounds__(NodalLayout<T, N>::THREADS, 1) nodal_mma_kerne
 #pragma unroll
           for (int F = 0; F < 4; ++F) {
             AT ah[M::AR], al[M::AR];
-            M::load_a(sf + F * MT * LF + ks * KS, LF, g, t, ah, al);
+            M::load_a(sfm + F * ET * LF + ks * KS, LF, g, t, ah, al);
             M::step(accl[F], ah, al, b);
           }
         }

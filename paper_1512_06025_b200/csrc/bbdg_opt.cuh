@@ -103,8 +103,7 @@ template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_group
   constexpr int g4[10] = {BBDG_OPT_NG4};
   constexpr int g8[10] = {BBDG_OPT_NG8};
   if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
-  if constexpr (OP == 1) return (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) ? BBDG_OPT_NG_TMEM
-                                                                                     : BBDG_OPT_NG_SURF;  // OP_SURFACE
+  if constexpr (OP == 1) return BBDG_OPT_NG_SURF;  // OP_SURFACE
   if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
   return SZ == 4 ? g4[N] : g8[N];
 }
@@ -126,7 +125,7 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // slot counts (items per thread, rounded up); a slot is "full" if every thread has an item
   static constexpr int NS_ITEMS = PPW * Nfp;
   static constexpr int SS = SURF ? (NS_ITEMS + 31) / 32 : 0;
-  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && OP != OP_VOLUME && N >= BBDG_OPT_TMEM_MIN_N;
+  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= BBDG_OPT_TMEM_MIN_N;
   // L0 lane offsets hoisted (registers, or TMEM in TMEM mode) -- else one LDS.128 per item
   static constexpr bool HOIST_L0 = SS <= 2 || TMH;
   static constexpr int SV1 = VOL ? (KE * Npm + GT - 1) / GT : 0;
@@ -179,15 +178,15 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int NG = ng_fit(227 * 1024) >= 1 ? ng_fit(227 * 1024) : 1;
   // hoisted per-thread tables parked in TMEM (fused fp32 kernels at high order, where
   // registers cap the group count): flat 32-bit word offsets of each table
-  static constexpr int SSa_ = SS > 0 ? SS : 1, SV1a_ = SV1 > 0 ? SV1 : 1, S3Ta_ = S3T > 0 ? S3T : 1;
-  // TMEM word map (per thread): S phase [own|fl, m|f|e, 3 L0 pairs, L0 coefficients x4, b!] per S slot;
-  // cascade [child e2 byte offset, child e0 byte offset] per item; V1 [4 child byte offsets (q tile),
-  // w byte offset, geometry byte offset, 1/beta! factor] per slot; V2 [4 parent byte offsets, 4 gather
-  // byte offsets, node, e << 16 | geometry byte offset, alpha!] + gather 1/beta! x4 per slot.
-  // Byte offsets are relative to the dynamic smem base (fixed buffers) or to the per-tile stage.
-  static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_L0C = H_SL0 + 3 * SSa_, H_FF = H_L0C + 4 * SSa_;
-  static constexpr int H_C3B = H_FF + SSa_, H_V1X = H_C3B + 2 * S3Ta_, H_V2X = H_V1X + 7 * SV1a_;
-  static constexpr int H_GF = H_V2X + 11 * SV2, NH = H_GF + 4 * SV2;
+  static constexpr int SSa_ = SS > 0 ? SS : 1, SV1a_ = SV1 > 0 ? SV1 : 1;
+  static constexpr int C3W = (S3T + 1) / 2 > 0 ? (S3T + 1) / 2 : 1;
+  static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);
+  static constexpr int H_V1C = H_C3 + C3W, H_V1W = H_V1C + 2 * SV1a_, H_V1F = H_V1W + SV1a_;
+  static constexpr int H_V2P = H_V1F + SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
+  static constexpr int H_V2F = H_V2M + SV2;
+  // per-point coefficients (TMEM mode only): L0 4-vector + b! per S slot, gather 1/beta! 4-vector per V2 slot
+  static constexpr int H_L0C = H_V2F + SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_, NH = H_GF + 4 * SV2;
+  static_assert(!TMH || NG * NH <= 512, "TMEM-parked tables exceed the 512 TMEM columns of an SM");
   static constexpr int tm_cols() {
     int c = 32;
     while (c < NG * NH) c *= 2;
@@ -494,6 +493,24 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       }
     }
 #pragma unroll
+    for (int x = 0; x < L::C3W; ++x) hx[L::H_C3 + x] = c3[x];
+#pragma unroll
+    for (int k = 0; k < SV1; ++k) {
+      hx[L::H_V1C + 2 * k] = v1c[k][0];
+      hx[L::H_V1C + 2 * k + 1] = v1c[k][1];
+      hx[L::H_V1W + k] = v1w[k];
+      hx[L::H_V1F + k] = __float_as_uint((float)v1f[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < SV2; ++k) {
+      hx[L::H_V2P + 2 * k] = v2p[k][0];
+      hx[L::H_V2P + 2 * k + 1] = v2p[k][1];
+      hx[L::H_V2G + 2 * k] = v2g[k][0];
+      hx[L::H_V2G + 2 * k + 1] = v2g[k][1];
+      hx[L::H_V2M + k] = v2m[k];
+      hx[L::H_V2F + k] = __float_as_uint((float)v2f[k]);
+    }
+#pragma unroll
     for (int k = 0; k < SS; ++k) {
       const int m = s_ef[k] & 0xff;
       const V4<T> c = l0c[m];
@@ -504,53 +521,12 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_FF + k] = __float_as_uint((float)ffac[m]);
     }
 #pragma unroll
-    for (int k = 0; k < SV1; ++k) {
-      uint32_t* h = hx + L::H_V1X + 7 * k;
-      h[0] = lo16(v1c[k][0]) * sz;
-      h[1] = hi16(v1c[k][0]) * sz;
-      h[2] = lo16(v1c[k][1]) * sz;
-      h[3] = hi16(v1c[k][1]) * sz;
-      if constexpr (L::WAOS) h[4] = (uint32_t)(reinterpret_cast<const unsigned char*>(sw + lo16(v1w[k])) - sm);
-      else h[4] = (uint32_t)(reinterpret_cast<const unsigned char*>(swp + lo16(v1w[k])) - sm);
-      h[5] = hi16(v1w[k]) * kGeoRec * sz;
-      h[6] = __float_as_uint((float)v1f[k]);
-    }
-#pragma unroll
     for (int k = 0; k < SV2; ++k) {
-      uint32_t* h = hx + L::H_V2X + 11 * k;
-      const uint32_t pp[4] = {lo16(v2p[k][0]), hi16(v2p[k][0]), lo16(v2p[k][1]), hi16(v2p[k][1])};
-      const uint32_t gg[4] = {lo16(v2g[k][0]), hi16(v2g[k][0]), lo16(v2g[k][1]), hi16(v2g[k][1])};
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        if constexpr (L::WAOS) h[x] = (uint32_t)(reinterpret_cast<const unsigned char*>(sw + pp[x]) - sm);
-        else h[x] = (uint32_t)(reinterpret_cast<const unsigned char*>(swp + pp[x]) - sm);
-        h[4 + x] = (uint32_t)(reinterpret_cast<const unsigned char*>(sW + 2 * gg[x]) - sm);
-      }
-      const uint32_t e = hi16(v2m[k]) >> 10;
-      h[8] = lo16(v2m[k]);
-      h[9] = (e << 16) | (e * kGeoRec * sz);
-      h[10] = __float_as_uint((float)v2f[k]);
       const V4<T> gf = gfac[hi16(v2m[k]) & 1023];
       hx[L::H_GF + 4 * k] = __float_as_uint((float)gf.x);
       hx[L::H_GF + 4 * k + 1] = __float_as_uint((float)gf.y);
       hx[L::H_GF + 4 * k + 2] = __float_as_uint((float)gf.z);
       hx[L::H_GF + 4 * k + 3] = __float_as_uint((float)gf.w);
-    }
-    if constexpr (L::SURF) {
-      static_for<1, N + 1>([&](auto J) {
-        constexpr int j = decltype(J)::value;
-        constexpr int ml = N - j, nhi = tri_dim(ml + 1);
-        const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
-#pragma unroll
-        for (int k = 0; k < L::s3_slots(j); ++k) {
-          const int x = L::s3_base(j) + k;
-          const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
-          const T* rd = Br + 32 * k + (c & 0xff);
-          const T* r3 = rd - ((c >> 8) & 0xff) + 2 * (ml + 2);
-          hx[L::H_C3B + 2 * x] = (uint32_t)(reinterpret_cast<const unsigned char*>(rd) - sm);
-          hx[L::H_C3B + 2 * x + 1] = (uint32_t)(reinterpret_cast<const unsigned char*>(r3) - sm);
-        }
-      });
     }
     tm_st<L::NH>(ta, hx);
     tm_wait_st();
@@ -561,34 +537,55 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   // reload one phase's tables from TMEM (no-op when they stay in registers)
   auto tm_load_s = [&] {
     if constexpr (L::TMH) {
-      uint32_t t[L::H_C3B];
-      tm_ld<L::H_C3B>(ta, t);
+      uint32_t t[2 * SSa];
+      tm_ld<2 * SSa>(ta + L::H_SOF, t);
+      uint32_t u[3 * SSa];
+      if constexpr (L::HOIST_L0) tm_ld<3 * SSa>(ta + L::H_SL0, u);
+      uint32_t cf[5 * SSa];
+      tm_ld<5 * SSa>(ta + L::H_L0C, cf);
       tm_wait_ld();
 #pragma unroll
       for (int k = 0; k < SS; ++k) {
-        s_of[k] = t[L::H_SOF + k];
-        s_ef[k] = t[L::H_SEF + k];
-        s_l0[k][0] = t[L::H_SL0 + 3 * k];
-        s_l0[k][1] = t[L::H_SL0 + 3 * k + 1];
-        s_l0[k][2] = t[L::H_SL0 + 3 * k + 2];
-        tl0[k] = V4<T>{(T)__uint_as_float(t[L::H_L0C + 4 * k]), (T)__uint_as_float(t[L::H_L0C + 4 * k + 1]),
-                       (T)__uint_as_float(t[L::H_L0C + 4 * k + 2]), (T)__uint_as_float(t[L::H_L0C + 4 * k + 3])};
-        tff[k] = (T)__uint_as_float(t[L::H_FF + k]);
+        tl0[k] = V4<T>{(T)__uint_as_float(cf[4 * k]), (T)__uint_as_float(cf[4 * k + 1]),
+                       (T)__uint_as_float(cf[4 * k + 2]), (T)__uint_as_float(cf[4 * k + 3])};
+        tff[k] = (T)__uint_as_float(cf[4 * SSa + k]);
+      }
+#pragma unroll
+      for (int k = 0; k < SS; ++k) {
+        s_of[k] = t[k];
+        s_ef[k] = t[SSa + k];
+        if constexpr (L::HOIST_L0) {
+          s_l0[k][0] = u[3 * k];
+          s_l0[k][1] = u[3 * k + 1];
+          s_l0[k][2] = u[3 * k + 2];
+        }
       }
     }
   };
-  auto tm_load_c3 = [&] {};   // TMEM mode: the cascade reads resolved offsets per level
-  // V1 / V2 tables with resolved byte offsets (TMEM mode)
-  uint32_t x1[L::TMH ? 7 * SV1a : 1], x2[L::TMH ? 11 * SV2 : 1];
+  auto tm_load_c3 = [&] {
+    if constexpr (L::TMH) {
+      tm_ld<L::C3W>(ta + L::H_C3, c3);
+      tm_wait_ld();
+    }
+  };
   auto tm_load_v1 = [&] {
     if constexpr (L::TMH) {
-      tm_ld<7 * SV1a>(ta + L::H_V1X, x1);
+      uint32_t t[4 * SV1a];
+      tm_ld<4 * SV1a>(ta + L::H_V1C, t);
       tm_wait_ld();
+#pragma unroll
+      for (int k = 0; k < SV1; ++k) {
+        v1c[k][0] = t[2 * k];
+        v1c[k][1] = t[2 * k + 1];
+        v1w[k] = t[2 * SV1a + k];
+        v1f[k] = (T)__uint_as_float(t[3 * SV1a + k]);
+      }
     }
   };
   auto tm_load_v2 = [&] {
     if constexpr (L::TMH) {
-      tm_ld<11 * SV2>(ta + L::H_V2X, x2);
+      uint32_t t[6 * SV2];
+      tm_ld<6 * SV2>(ta + L::H_V2P, t);
       uint32_t gq[4 * SV2];
       tm_ld<4 * SV2>(ta + L::H_GF, gq);
       tm_wait_ld();
@@ -596,6 +593,15 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       for (int k = 0; k < SV2; ++k)
         tgf[k] = V4<T>{(T)__uint_as_float(gq[4 * k]), (T)__uint_as_float(gq[4 * k + 1]),
                        (T)__uint_as_float(gq[4 * k + 2]), (T)__uint_as_float(gq[4 * k + 3])};
+#pragma unroll
+      for (int k = 0; k < SV2; ++k) {
+        v2p[k][0] = t[2 * k];
+        v2p[k][1] = t[2 * k + 1];
+        v2g[k][0] = t[2 * SV2 + 2 * k];
+        v2g[k][1] = t[2 * SV2 + 2 * k + 1];
+        v2m[k] = t[4 * SV2 + k];
+        v2f[k] = (T)__uint_as_float(t[5 * SV2 + k]);
+      }
     }
   };
 
@@ -781,29 +787,18 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       static_for<1, N + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
-        constexpr int NSL = L::s3_slots(j);
         const T kap = T(cascade_kappa(N, j));
         T* const Bw = sW + 8 * KE * layer_off(N, j) + 2 * wg * PPW * nlo + lane;
         const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
-        uint32_t cb[L::TMH ? 2 * NSL : 1];
-        if constexpr (L::TMH) tm_ld<2 * NSL>(ta + L::H_C3B + 2 * L::s3_base(j), cb);
         __syncwarp();
-        if constexpr (L::TMH) tm_wait_ld();
-        static_for<0, NSL>([&](auto KK) {
+        static_for<0, L::s3_slots(j)>([&](auto KK) {
           constexpr int k = decltype(KK)::value;
           constexpr int x = L::s3_base(j) + k;
           slot<k, 32, L::s3_items(j)>(lane, [&] {
-            if constexpr (L::TMH) {
-              // children at resolved smem byte offsets: e2 / e1 (pair-adjacent) and e0
-              const T* rd = reinterpret_cast<const T*>(sm + cb[2 * k]);
-              const T* r3 = reinterpret_cast<const T*>(sm + cb[2 * k + 1]);
-              Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[0]);
-            } else {
-              const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
-              const T* rd = Br + 32 * k + (c & 0xff);
-              const T* r3 = rd - ((c >> 8) & 0xff);
-              Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
-            }
+            const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+            const T* rd = Br + 32 * k + (c & 0xff);
+            const T* r3 = rd - ((c >> 8) & 0xff);
+            Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
           });
         });
       });
@@ -815,41 +810,22 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       static_for<0, SV1>([&](auto KK) {
         constexpr int k = decltype(KK)::value;
         slot<k, GT, KE * Npm>(ltid, [&] {
-          const T* gr;
-          T f1;
-          int c0 = 0, c1 = 0, c2 = 0, c3i = 0;
-          const uint32_t* h = x1 + (L::TMH ? 7 * k : 0);
-          if constexpr (L::TMH) {
-            gr = (KE == 1) ? sgeo : reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(sgeo) + h[5]);
-            f1 = (T)__uint_as_float(h[6]);
-          } else {
-            const int e = (KE == 1) ? 0 : (int)hi16(v1w[k]);
-            gr = sgeo + e * kGeoRec;
-            f1 = v1f[k];
-            c0 = lo16(v1c[k][0]), c1 = hi16(v1c[k][0]), c2 = lo16(v1c[k][1]), c3i = hi16(v1c[k][1]);
-          }
+          const int e = (KE == 1) ? 0 : (int)hi16(v1w[k]);
+          const T* gr = sgeo + e * kGeoRec;
+          const int c0 = lo16(v1c[k][0]), c1 = hi16(v1c[k][0]), c2 = lo16(v1c[k][1]), c3i = hi16(v1c[k][1]);
           T d[4][3];
 #pragma unroll
           for (int F = 0; F < 4; ++F) {
-            T x0, x1v, x2, x3;
-            if constexpr (L::TMH) {
-              const unsigned char* qf = reinterpret_cast<const unsigned char*>(sq + F * S);
-              x0 = *reinterpret_cast<const T*>(qf + h[0]);
-              x1v = *reinterpret_cast<const T*>(qf + h[1]);
-              x2 = *reinterpret_cast<const T*>(qf + h[2]);
-              x3 = *reinterpret_cast<const T*>(qf + h[3]);
-            } else {
-              const T* qe = sq + F * S;
-              x0 = qe[c0], x1v = qe[c1], x2 = qe[c2], x3 = qe[c3i];
-            }
+            const T* qe = sq + F * S;
+            const T x0 = qe[c0], x1 = qe[c1], x2 = qe[c2], x3 = qe[c3i];
             // children b+e_0..b+e_3: Delta_m = q[b+e_{m+1}] - q[b+e_0]  (exactly 0 for constant states)
-            d[F][0] = x1v - x0;
+            d[F][0] = x1 - x0;
             d[F][1] = x2 - x0;
             d[F][2] = x3 - x0;
           }
           const T* G = gr + 26;   // rst_dx[m][i] = G[3m+i]
-          const T sr = -gr[25] * f1;   // -(1/rho)/2 / beta!
-          const T sk = -gr[24] * f1;   // -kappa/2 / beta!
+          const T sr = -gr[25] * v1f[k];   // -(1/rho)/2 / beta!
+          const T sk = -gr[24] * v1f[k];   // -kappa/2 / beta!
           T wu[3];
 #pragma unroll
           for (int c = 0; c < 3; ++c) wu[c] = sr * (G[c] * d[0][0] + G[3 + c] * d[0][1] + G[6 + c] * d[0][2]);
@@ -857,10 +833,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
 #pragma unroll
           for (int c = 0; c < 3; ++c) div += G[c] * d[1 + c][0] + G[3 + c] * d[1 + c][1] + G[6 + c] * d[1 + c][2];
           if constexpr (L::WAOS) {
-            V4<T>* wd = L::TMH ? reinterpret_cast<V4<T>*>(sm + h[4]) : sw + lo16(v1w[k]);
-            *wd = V4<T>{sk * div, wu[0], wu[1], wu[2]};
+            sw[lo16(v1w[k])] = V4<T>{sk * div, wu[0], wu[1], wu[2]};
           } else {
-            T* w = L::TMH ? reinterpret_cast<T*>(sm + h[4]) : swp + lo16(v1w[k]);
+            T* w = swp + lo16(v1w[k]);
             w[0] = sk * div;
 #pragma unroll
             for (int c = 0; c < 3; ++c) w[(1 + c) * KE * NWS] = wu[c];
@@ -877,61 +852,35 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     static_for<0, SV2>([&](auto KK) {
       constexpr int k = decltype(KK)::value;
       slot<k, GT, KE * Np>(ltid, [&] {
-        const uint32_t* h = x2 + (L::TMH ? 11 * k : 0);
-        const int t = L::TMH ? (int)h[8] : (int)lo16(v2m[k]);
-        const int e = (KE == 1) ? 0 : (L::TMH ? (int)(h[9] >> 16) : (int)(hi16(v2m[k]) >> 10));
-        const int a = hi16(v2m[k]) & 1023;
-        const T* gr = L::TMH ? reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(sgeo) + (h[9] & 0xffffu))
-                             : sgeo + e * kGeoRec;
+        const int t = lo16(v2m[k]);
+        const int e = (KE == 1) ? 0 : (int)(hi16(v2m[k]) >> 10), a = hi16(v2m[k]) & 1023;
+        const T* gr = sgeo + e * kGeoRec;
         (void)gr;
         (void)a;
         T r[4];
         if constexpr (L::VOL) {
-          const T f2 = L::TMH ? (T)__uint_as_float(h[10]) : v2f[k];
+          const int p0 = lo16(v2p[k][0]), p1 = hi16(v2p[k][0]), p2 = lo16(v2p[k][1]), p3 = hi16(v2p[k][1]);
           if constexpr (L::WAOS) {
-            V4<T> w0, w1, w2, w3;
-            if constexpr (L::TMH) {
-              w0 = *reinterpret_cast<const V4<T>*>(sm + h[0]);
-              w1 = *reinterpret_cast<const V4<T>*>(sm + h[1]);
-              w2 = *reinterpret_cast<const V4<T>*>(sm + h[2]);
-              w3 = *reinterpret_cast<const V4<T>*>(sm + h[3]);
-            } else {
-              w0 = sw[lo16(v2p[k][0])], w1 = sw[hi16(v2p[k][0])], w2 = sw[lo16(v2p[k][1])], w3 = sw[hi16(v2p[k][1])];
-            }
-            r[0] = f2 * ((w0.x + w1.x) + (w2.x + w3.x));
-            r[1] = f2 * ((w0.y + w1.y) + (w2.y + w3.y));
-            r[2] = f2 * ((w0.z + w1.z) + (w2.z + w3.z));
-            r[3] = f2 * ((w0.w + w1.w) + (w2.w + w3.w));
+            const V4<T> w0 = sw[p0], w1 = sw[p1], w2 = sw[p2], w3 = sw[p3];
+            r[0] = v2f[k] * ((w0.x + w1.x) + (w2.x + w3.x));
+            r[1] = v2f[k] * ((w0.y + w1.y) + (w2.y + w3.y));
+            r[2] = v2f[k] * ((w0.z + w1.z) + (w2.z + w3.z));
+            r[3] = v2f[k] * ((w0.w + w1.w) + (w2.w + w3.w));
           } else {
-            const T *w0, *w1, *w2, *w3;
-            if constexpr (L::TMH) {
-              w0 = reinterpret_cast<const T*>(sm + h[0]), w1 = reinterpret_cast<const T*>(sm + h[1]);
-              w2 = reinterpret_cast<const T*>(sm + h[2]), w3 = reinterpret_cast<const T*>(sm + h[3]);
-            } else {
-              w0 = swp + lo16(v2p[k][0]), w1 = swp + hi16(v2p[k][0]), w2 = swp + lo16(v2p[k][1]),
-              w3 = swp + hi16(v2p[k][1]);
-            }
 #pragma unroll
             for (int F = 0; F < 4; ++F) {
-              const int o = F * KE * NWS;
-              r[F] = f2 * ((w0[o] + w1[o]) + (w2[o] + w3[o]));
+              const T* w = swp + F * KE * NWS;
+              r[F] = v2f[k] * ((w[p0] + w[p1]) + (w[p2] + w[p3]));
             }
           }
         }
         if constexpr (L::SURF) {
+          const int g0 = lo16(v2g[k][0]), g1 = hi16(v2g[k][0]), g2 = lo16(v2g[k][1]), g3 = hi16(v2g[k][1]);
           V4<T> gf;
-          P2<T> w0, w1, w2, w3;
-          if constexpr (L::TMH) {
-            gf = tgf[k];
-            w0 = *reinterpret_cast<const P2<T>*>(sm + h[4]);
-            w1 = *reinterpret_cast<const P2<T>*>(sm + h[5]);
-            w2 = *reinterpret_cast<const P2<T>*>(sm + h[6]);
-            w3 = *reinterpret_cast<const P2<T>*>(sm + h[7]);
-          } else {
-            gf = gfac[a];
-            const P2<T>* W2 = reinterpret_cast<const P2<T>*>(sW);
-            w0 = W2[lo16(v2g[k][0])], w1 = W2[hi16(v2g[k][0])], w2 = W2[lo16(v2g[k][1])], w3 = W2[hi16(v2g[k][1])];
-          }
+          if constexpr (L::TMH) gf = tgf[k];
+          else gf = gfac[a];
+          const P2<T>* W2 = reinterpret_cast<const P2<T>*>(sW);
+          const P2<T> w0 = W2[g0], w1 = W2[g1], w2 = W2[g2], w3 = W2[g3];
           const T sp = gf.x * w0.x + gf.y * w1.x + gf.z * w2.x + gf.w * w3.x;
           const T u0 = gf.x * w0.y, u1 = gf.y * w1.y, u2 = gf.z * w2.y, u3 = gf.w * w3.y;
           const V4<T> n0 = *reinterpret_cast<const V4<T>*>(gr + 0);
@@ -955,7 +904,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
             r[3] = s3;
           }
         }
-        if (KE == 1 || e < nv) {
+        if (KE == 1 || (int)(hi16(v2m[k]) >> 10) < nv) {
           if constexpr (OP == OP_STAGE) {
             // res = A res + dt rhs; q_out = q_in + B res   (reference solver.py:211-213)
 #pragma unroll

@@ -103,7 +103,8 @@ template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_group
   constexpr int g4[10] = {BBDG_OPT_NG4};
   constexpr int g8[10] = {BBDG_OPT_NG8};
   if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
-  if constexpr (OP == 1) return BBDG_OPT_NG_SURF;  // OP_SURFACE
+  if constexpr (OP == 1) return (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) ? BBDG_OPT_NG_TMEM
+                                                                                     : BBDG_OPT_NG_SURF;  // OP_SURFACE
   if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
   return SZ == 4 ? g4[N] : g8[N];
 }
@@ -125,7 +126,7 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // slot counts (items per thread, rounded up); a slot is "full" if every thread has an item
   static constexpr int NS_ITEMS = PPW * Nfp;
   static constexpr int SS = SURF ? (NS_ITEMS + 31) / 32 : 0;
-  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && (OP == OP_STAGE || OP == OP_RHS) && N >= BBDG_OPT_TMEM_MIN_N;
+  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && OP != OP_VOLUME && N >= BBDG_OPT_TMEM_MIN_N;
   // L0 lane offsets hoisted (registers, or TMEM in TMEM mode) -- else one LDS.128 per item
   static constexpr bool HOIST_L0 = SS <= 2 || TMH;
   static constexpr int SV1 = VOL ? (KE * Npm + GT - 1) / GT : 0;

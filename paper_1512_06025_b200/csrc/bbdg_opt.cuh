@@ -784,24 +784,44 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         });
       });
       // ------------------------------------------------------------- S3: reduction cascade (Alg. 1)
+      // Levels that fit one slot keep their values in a register (item i in lane i); a level
+      // whose parent level also fits one slot reads its three children with shuffles instead
+      // of shared memory (its values are still stored for the gather).
       tm_load_c3();
+      T prev = T(0);
       static_for<1, N + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
+        constexpr bool ONE = L::s3_slots(j) == 1;
+        constexpr bool SHF = ONE && j >= 2 && L::s3_slots(j - 1) == 1;
         const T kap = T(cascade_kappa(N, j));
         T* const Bw = sW + 8 * KE * layer_off(N, j) + 2 * wg * PPW * nlo + lane;
         const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
-        __syncwarp();
-        static_for<0, L::s3_slots(j)>([&](auto KK) {
-          constexpr int k = decltype(KK)::value;
-          constexpr int x = L::s3_base(j) + k;
-          slot<k, 32, L::s3_items(j)>(lane, [&] {
-            const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
-            const T* rd = Br + 32 * k + (c & 0xff);
-            const T* r3 = rd - ((c >> 8) & 0xff);
-            Bw[32 * k] = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
+        if constexpr (SHF) {
+          constexpr int x = L::s3_base(j);
+          const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+          const int i2 = lane + (int)(c & 0xff), i0 = i2 - (int)((c >> 8) & 0xff) + 2 * (ml + 2);
+          const T a = __shfl_sync(0xffffffffu, prev, i2 & 31);
+          const T b = __shfl_sync(0xffffffffu, prev, (i2 + 2) & 31);
+          const T d = __shfl_sync(0xffffffffu, prev, i0 & 31);
+          const T val = kap * ((a + b) + d);
+          if (lane < L::s3_items(j)) Bw[0] = val;
+          prev = val;
+        } else {
+          __syncwarp();
+          static_for<0, L::s3_slots(j)>([&](auto KK) {
+            constexpr int k = decltype(KK)::value;
+            constexpr int x = L::s3_base(j) + k;
+            slot<k, 32, L::s3_items(j)>(lane, [&] {
+              const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+              const T* rd = Br + 32 * k + (c & 0xff);
+              const T* r3 = rd - ((c >> 8) & 0xff);
+              const T val = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
+              Bw[32 * k] = val;
+              if constexpr (ONE) prev = val;
+            });
           });
-        });
+        }
       });
     }
 

@@ -102,6 +102,19 @@ int bbdg_lsrk_update(int dtype, int64_t n, void* q, void* res, const void* rhs, 
  * the result in q.  q_tmp and res are caller-owned (4,K,Np) scratch. */
 int bbdg_step(bbdg_ctx* ctx, void* q, void* q_tmp, void* res, double dt, int lift_mode, void* stream);
 
+/* lsrk4_step on a host state (solver.py:196-214 called with a numpy q): H2D of
+ * host_q, the five stages and the D2H of the result into host_q, pipelined over
+ * element chunks bounds[0..nchunks] (bounds[0] = 0, bounds[nchunks] = K) whose
+ * neighbours lie within `reach` chunks, so the copies in both directions overlap
+ * the stages of other chunks.  q, q_tmp, res are (4,K,Np) device scratch; the
+ * copies run on h2d_stream / d2h_stream, the kernels on `stream`, which is
+ * joined with both before return (host_q is final once `stream` completes).
+ * host_q should be pinned for the copies to overlap.  Results are bitwise
+ * equal to bbdg_step. */
+int bbdg_step_host(bbdg_ctx* ctx, void* host_q, void* q, void* q_tmp, void* res, double dt, int lift_mode,
+                   const int64_t* bounds, int nchunks, int reach, void* stream, void* h2d_stream,
+                   void* d2h_stream);
+
 /* Pack the face traces of (elem, face) pairs (device int32 (n,2)) into
  * sendbuf (4, n, Nfp) in each face's own canonical order (halo send side). */
 int bbdg_halo_pack(bbdg_ctx* ctx, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream);

@@ -562,6 +562,93 @@ int bbdg_step(bbdg_ctx* c, void* q, void* q_tmp, void* res, double dt, int lift,
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "final stage copy");
 }
 
+// lsrk4_step on a HOST state: the element range is cut into chunks whose neighbours lie within
+// `reach` chunks (banded element numbering, e.g. cube_mesh's x-slabs).  Stage s of chunk i runs in
+// slot t = i + reach (s-1), stages ascending within a slot: stage s-1 of chunks i-reach..i+reach
+// then precedes it in stream order (the last of them, chunk i+reach, earlier in the same slot) --
+// both its reads of q_{s-1} and the last reads of the q_{s-2} values it overwrites (ping-pong).
+// Chunk i's H2D (h2d stream) gates stage 1 of chunk i-reach; chunk i's D2H (d2h stream) follows
+// its stage 5, so both copy directions overlap the stages of the other chunks.  The result
+// (stage 5 writes q_tmp) goes straight to the host array; the stream `stream` is joined with
+// both copy streams before return, so work queued after the call sees host_q complete.
+int bbdg_step_host(bbdg_ctx* c, void* host_q, void* q, void* q_tmp, void* res, double dt, int lift,
+                   const int64_t* bounds, int nchunks, int reach, void* stream, void* h2d_stream, void* d2h_stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!host_q || !q || !q_tmp || !res || !bounds) return set_error(BBDG_ERR_ARG, "null pointer");
+  if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  if (nchunks < 1 || reach < 0 || bounds[0] != 0 || bounds[nchunks] != c->K)
+    return set_error(BBDG_ERR_ARG, "chunk bounds must cover [0, K)");
+  for (int i = 0; i < nchunks; ++i)
+    if (bounds[i + 1] <= bounds[i]) return set_error(BBDG_ERR_ARG, "chunk bounds must increase");
+  if (c->nhalo) return set_error(BBDG_ERR_ARG, "host-pipelined step on a partitioned context");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream), hs = static_cast<cudaStream_t>(h2d_stream),
+               ds = static_cast<cudaStream_t>(d2h_stream);
+  const size_t sz = c->dtype == BBDG_F32 ? 4 : 8, plane = (size_t)c->K * c->Np * sz;
+  std::vector<cudaEvent_t> ev(2 * nchunks + 2, nullptr);
+  int rc = BBDG_OK;
+  auto fail = [&](cudaError_t e, const char* where) {
+    rc = set_cuda_error(e, where);
+    return rc;
+  };
+  for (auto& e : ev)
+    if (cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) {
+      fail(r, "event create");
+      break;
+    }
+  cudaEvent_t* h2d_done = ev.data();
+  cudaEvent_t* st5_done = ev.data() + nchunks;
+  cudaEvent_t start = ev[2 * nchunks], d2h_all = ev[2 * nchunks + 1];
+  auto copy_chunk = [&](char* dst, const char* src, int i, cudaMemcpyKind kind, cudaStream_t s) {
+    const size_t off = (size_t)bounds[i] * c->Np * sz, len = (size_t)(bounds[i + 1] - bounds[i]) * c->Np * sz;
+    for (int F = 0; F < 4 && rc == BBDG_OK; ++F)
+      if (cudaError_t r = cudaMemcpyAsync(dst + F * plane + off, src + F * plane + off, len, kind, s))
+        fail(r, "chunk copy");
+  };
+  // the copy streams start after the work already queued on `stream` (buffers may be in use)
+  if (rc == BBDG_OK) {
+    if (cudaError_t r = cudaEventRecord(start, cs)) fail(r, "event record");
+    else if ((r = cudaStreamWaitEvent(hs, start, 0)) || (r = cudaStreamWaitEvent(ds, start, 0))) fail(r, "wait");
+  }
+  if (rc == BBDG_OK)
+    if (cudaError_t r = cudaMemsetAsync(res, 0, 4 * plane, cs)) fail(r, "res zeroing");
+  for (int i = 0; i < nchunks && rc == BBDG_OK; ++i) {
+    copy_chunk(static_cast<char*>(q), static_cast<const char*>(host_q), i, cudaMemcpyHostToDevice, hs);
+    if (rc == BBDG_OK)
+      if (cudaError_t r = cudaEventRecord(h2d_done[i], hs)) fail(r, "event record");
+  }
+  void* buf[2] = {q, q_tmp};
+  const int lag = reach, slots = nchunks + 4 * lag;
+  for (int t = 0; t < slots && rc == BBDG_OK; ++t) {
+    for (int s = 0; s < 5 && rc == BBDG_OK; ++s) {
+      const int i = t - lag * s;
+      if (i < 0 || i >= nchunks) continue;
+      if (s == 0) {
+        const int need = i + reach < nchunks ? i + reach : nchunks - 1;
+        if (cudaError_t r = cudaStreamWaitEvent(cs, h2d_done[need], 0)) {
+          fail(r, "wait");
+          break;
+        }
+      }
+      rc = bbdg_lsrk_stage_range(c, buf[s & 1], buf[(s + 1) & 1], res, lift, kRK4A[s], kRK4B[s], dt, bounds[i],
+                                 bounds[i + 1], stream);
+      if (rc == BBDG_OK && s == 4) {
+        cudaError_t r = cudaEventRecord(st5_done[i], cs);
+        if (!r) r = cudaStreamWaitEvent(ds, st5_done[i], 0);
+        if (r) fail(r, "event");
+        else copy_chunk(static_cast<char*>(host_q), static_cast<const char*>(q_tmp), i, cudaMemcpyDeviceToHost, ds);
+      }
+    }
+  }
+  if (rc == BBDG_OK) {
+    cudaError_t r = cudaEventRecord(d2h_all, ds);
+    if (!r) r = cudaStreamWaitEvent(cs, d2h_all, 0);
+    if (r) fail(r, "join");
+  }
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);   // released once the queued work that uses it completes
+  return rc;
+}
+
 int bbdg_halo_pack(bbdg_ctx* c, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream) {
   if (!c || (n > 0 && (!q || !sendbuf || !faces))) return set_error(BBDG_ERR_ARG, "bad halo pack arguments");
   if (n == 0) return BBDG_OK;

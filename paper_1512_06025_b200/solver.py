@@ -326,6 +326,65 @@ def _device_update(q_dev, res_dev, k_dev, a, b, dt):
                "bbdg_lsrk_update")
 
 
+def host_chunk_plan(etoe, Np: int, itemsize: int, max_chunks: int = 48, min_state_bytes: int = 32 << 20,
+                    chunk: int | None = None):
+    """Element chunks for the host-pipelined step (``bbdg_step_host``): (bounds, reach) or None.
+
+    Chunks are at least as long as the largest neighbour-index distance of the
+    mesh (so a banded numbering such as cube_mesh's x-slabs gives reach 1) and
+    at most ``max_chunks`` of them; ``reach`` is the exact largest chunk distance
+    between an element and any neighbour.  None when the state is too small for
+    chunking to pay, or the numbering is not banded enough to pipeline.
+    """
+    etoe = np.asarray(etoe)
+    K = etoe.shape[0]
+    if 4 * K * Np * itemsize < min_state_bytes:
+        return None
+    idx = np.arange(K, dtype=np.int64)[:, None]
+    band = int(np.abs(etoe.astype(np.int64) - idx).max()) if K else 0
+    csize = chunk if chunk is not None else max(band, -(-K // max_chunks), 1)
+    nch = -(-K // csize)
+    if nch < 3:
+        return None
+    cid = etoe.astype(np.int64) // csize
+    own = idx // csize
+    reach = int(np.abs(cid - own).max())
+    if 4 * (reach + 1) >= nch:   # pipeline fill longer than the work: nothing overlaps
+        return None
+    bounds = np.minimum(np.arange(nch + 1, dtype=np.int64) * csize, K)
+    return bounds, reach
+
+
+def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -> bool:
+    """Pipelined H2D + five stages + D2H of a pinned host state (bbdg_step_host); False if not applicable."""
+    if system._plan is not None or not isinstance(q_host, np.ndarray) or not q_host.flags.c_contiguous \
+            or not q_host.flags.writeable or q_host.dtype != np.dtype(system.dtype):
+        return False
+    torch = _torch()
+    if not torch.from_numpy(q_host).is_pinned():
+        return False   # pageable copies are synchronous: nothing would overlap
+    if not hasattr(system, "_chunks"):
+        etoe = system.mesh.etoe
+        if _is_tensor(etoe):
+            etoe = etoe.cpu().numpy()
+        system._chunks = host_chunk_plan(etoe, system.ops.Np, np.dtype(system.dtype).itemsize)
+    if system._chunks is None:
+        return False
+    bounds, reach = system._chunks
+    if not hasattr(system, "_copy_streams"):
+        system._copy_streams = (torch.cuda.Stream(), torch.cuda.Stream())
+    hs, ds = system._copy_streams
+    q = system.empty_state()
+    tmp, r = torch.empty_like(q), torch.empty_like(q)
+    cs = torch.cuda.current_stream()
+    _lib.check(system._lib.bbdg_step_host(system._ctx, q_host.ctypes.data, q.data_ptr(), tmp.data_ptr(), r.data_ptr(),
+                                          float(dt), system._lift_id(lift), bounds.ctypes.data, len(bounds) - 1,
+                                          int(reach), cs.cuda_stream, hs.cuda_stream, ds.cuda_stream),
+               "bbdg_step_host")
+    cs.synchronize()   # host_q holds the new state (reference: in place on return)
+    return True
+
+
 def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorized", res=None) -> FieldState:
     """One five-stage LSRK4 step, in place on state.q (reference solver.py:196-214).
 
@@ -341,6 +400,9 @@ def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorize
         system._check(state)
         lift = system._nodal_mode(lift_mode)
         system._lift_id(lift)
+        # pinned numpy state, fresh res: copies in both directions overlap the stages chunk by chunk
+        if res is None and _host_step(system, state.q, dt, lift):
+            return FieldState(state.q, state.basis, t0 + dt)
         q = system.to_device(state.q)
         r = system.to_device(res) if res is not None else torch.empty_like(q)
         tmp = torch.empty_like(q)

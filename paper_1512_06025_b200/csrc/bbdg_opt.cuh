@@ -90,6 +90,20 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_ke() {
 #ifndef BBDG_OPT_NG_SURF
 #define BBDG_OPT_NG_SURF 4
 #endif
+// cascade levels whose parent level spans <= this many slots read their children by shuffles
+// (per order; measured: more than one slot loses in fp32 -- 3 slots: sweep 136 -> 127 GDOF/s --
+// and wins only at N = 7, 9 in fp64)
+#ifndef BBDG_OPT_SHF4
+#define BBDG_OPT_SHF4 0, 1, 1, 1, 1, 1, 1, 1, 1, 1
+#endif
+#ifndef BBDG_OPT_SHF8
+#define BBDG_OPT_SHF8 0, 1, 1, 1, 1, 1, 1, 2, 1, 2
+#endif
+template <int N, int SZ> __host__ __device__ constexpr int opt_shf_slots() {
+  constexpr int s4[10] = {BBDG_OPT_SHF4};
+  constexpr int s8[10] = {BBDG_OPT_SHF8};
+  return SZ == 4 ? s4[N] : s8[N];
+}
 #ifndef BBDG_OPT_TMEM
 #define BBDG_OPT_TMEM 1
 #endif
@@ -323,6 +337,18 @@ __device__ __forceinline__ uint32_t pk(uint32_t a, uint32_t b) { return a | (b <
 
 // run f() for slot K of a phase with `count` items spread over `width` threads;
 // full slots are unguarded at compile time
+// value of item x (in slot x / 32, lane x % 32) of a level held one slot per register:
+// one shuffle per slot, the owning slot's result kept (all lanes must call it)
+template <int PS, typename T> __device__ __forceinline__ T warp_gather(const T* v, int x) {
+  T r = __shfl_sync(0xffffffffu, v[0], x & 31);
+#pragma unroll
+  for (int s = 1; s < PS; ++s) {
+    const T t = __shfl_sync(0xffffffffu, v[s], x & 31);
+    if ((x >> 5) == s) r = t;
+  }
+  return r;
+}
+
 template <int K, int WIDTH, int COUNT, class F> __device__ __forceinline__ void slot(int idx, F&& f) {
   if constexpr ((K + 1) * WIDTH <= COUNT) {
     f();
@@ -788,25 +814,38 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       // whose parent level also fits one slot reads its three children with shuffles instead
       // of shared memory (its values are still stored for the gather).
       tm_load_c3();
-      T prev = T(0);
+      // Every level keeps its values in registers too (item i = lane + 32 k in prev[k]); a level
+      // whose parent level spans at most BBDG_OPT_SHF_SLOTS slots reads its three children by
+      // warp shuffles (one per parent slot, a SHFL costs ~1/4 of an LDS on the shared-memory pipe)
+      // instead of shared memory.  The values are still stored for the lift gather.
+      constexpr int PSM = L::s3_slots(1);
+      T prev[PSM];
+#pragma unroll
+      for (int k = 0; k < PSM; ++k) prev[k] = T(0);
       static_for<1, N + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr int ml = N - j, nlo = tri_dim(ml), nhi = tri_dim(ml + 1);
-        constexpr bool ONE = L::s3_slots(j) == 1;
-        constexpr bool SHF = ONE && j >= 2 && L::s3_slots(j - 1) == 1;
+        constexpr int PS = j >= 2 ? L::s3_slots(j - 1) : 0;
+        constexpr bool SHF = j >= 2 && PS <= opt_shf_slots<N, sz>();
         const T kap = T(cascade_kappa(N, j));
         T* const Bw = sW + 8 * KE * layer_off(N, j) + 2 * wg * PPW * nlo + lane;
         const T* const Br = sW + 8 * KE * layer_off(N, j - 1) + 2 * wg * PPW * nhi + lane;
         if constexpr (SHF) {
-          constexpr int x = L::s3_base(j);
-          const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
-          const int i2 = lane + (int)(c & 0xff), i0 = i2 - (int)((c >> 8) & 0xff) + 2 * (ml + 2);
-          const T a = __shfl_sync(0xffffffffu, prev, i2 & 31);
-          const T b = __shfl_sync(0xffffffffu, prev, (i2 + 2) & 31);
-          const T d = __shfl_sync(0xffffffffu, prev, i0 & 31);
-          const T val = kap * ((a + b) + d);
-          if (lane < L::s3_items(j)) Bw[0] = val;
-          prev = val;
+          T cur[PSM];
+          static_for<0, L::s3_slots(j)>([&](auto KK) {
+            constexpr int k = decltype(KK)::value;
+            constexpr int x = L::s3_base(j) + k;
+            const uint32_t c = c3[x >> 1] >> (16 * (x & 1));
+            const int i2 = lane + 32 * k + (int)(c & 0xff), i0 = i2 - (int)((c >> 8) & 0xff) + 2 * (ml + 2);
+            const T a = warp_gather<PS>(prev, i2);
+            const T b = warp_gather<PS>(prev, i2 + 2);
+            const T d = warp_gather<PS>(prev, i0);
+            const T val = kap * ((a + b) + d);
+            if (lane + 32 * k < L::s3_items(j)) Bw[32 * k] = val;
+            cur[k] = val;
+          });
+#pragma unroll
+          for (int k = 0; k < L::s3_slots(j); ++k) prev[k] = cur[k];
         } else {
           __syncwarp();
           static_for<0, L::s3_slots(j)>([&](auto KK) {
@@ -818,7 +857,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
               const T* r3 = rd - ((c >> 8) & 0xff);
               const T val = kap * ((rd[0] + rd[2]) + r3[2 * (ml + 2)]);
               Bw[32 * k] = val;
-              if constexpr (ONE) prev = val;
+              prev[k] = val;
             });
           });
         }

@@ -5,19 +5,14 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"vH", "vI"}
+F64 = {"s1d", "s2d", "s4d"}
 VARIANTS = {
-    "vJ": ["-DBBDG_OPT_NG_TMEM=6"],
-    "vK": ["-DBBDG_OPT_NG_TMEM=6", "-DBBDG_OPT_TMEM_MIN_N=2"],
-    "vH": ["-DBBDG_OPT_KE8=0,16,12,6,4,3,2,2,1,1"],
-    "vI": ["-DBBDG_OPT_KE8=0,32,24,12,6,4,3,2,2,1"],
-    "vB": ["-DBBDG_OPT_KE4=0,16,12,6,4,2,2,1,1,1", "-DBBDG_OPT_NG4=0,8,8,8,6,6,6,4,4,4"],
-    "vC": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,4,4,4,4,4,4,4,3,4"],
-    "vD": ["-DBBDG_OPT_KE4=0,8,6,4,2,2,1,1,1,1", "-DBBDG_OPT_NG4=0,8,8,8,8,8,8,6,6,5"],
-    "vE": ["-DBBDG_OPT_KE4=0,32,24,12,6,6,4,3,2,2", "-DBBDG_OPT_NG4=0,4,4,4,4,4,4,3,3,3"],
-    "vS": ["-DBBDG_OPT_NG_SURF=6"],
-    "vF": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,5,5,5,5,5,5,5,3,5"],
-    "vG": ["-DBBDG_OPT_KE4=0,32,24,12,6,4,3,2,2,1", "-DBBDG_OPT_NG4=0,6,6,6,6,6,6,6,4,6"],
+    "s1": ["-DBBDG_OPT_SHF_SLOTS=1"],
+    "s2": ["-DBBDG_OPT_SHF_SLOTS=2"],
+    "s4": ["-DBBDG_OPT_SHF_SLOTS=4"],
+    "s2d": ["-DBBDG_OPT_SHF_SLOTS=2"],
+    "s1d": ["-DBBDG_OPT_SHF_SLOTS=1"],
+    "s4d": ["-DBBDG_OPT_SHF_SLOTS=4"],
 }
 
 if __name__ == "__main__":

@@ -110,6 +110,21 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_shf_slots() {
 #ifndef BBDG_OPT_NG_TMEM
 #define BBDG_OPT_NG_TMEM 5   // groups of the fused fp32 kernels whose hoisted tables live in TMEM
 #endif
+#ifndef BBDG_OPT_RES_GLOBAL
+#define BBDG_OPT_RES_GLOBAL 1   // fp64 stage: the LSRK register is read straight from HBM in the epilogue
+#endif
+#ifndef BBDG_OPT_RES_GLOBAL_MIN_N
+#define BBDG_OPT_RES_GLOBAL_MIN_N 3   // (measured: N = 1, 2 lose 3-9 %; they are not smem-bound)
+#endif
+#ifndef BBDG_OPT_TMEM64
+#define BBDG_OPT_TMEM64 1   // fp64 fused kernels park their offset tables in TMEM too (coefficients stay in smem)
+#endif
+#ifndef BBDG_OPT_NG_TMEM8
+#define BBDG_OPT_NG_TMEM8 4
+#endif
+#ifndef BBDG_OPT_TMEM64_MIN_N
+#define BBDG_OPT_TMEM64_MIN_N 4
+#endif
 #ifndef BBDG_OPT_TMEM_MIN_N
 #define BBDG_OPT_TMEM_MIN_N 4   // (measured: no gain below N = 4, where registers do not bind)
 #endif
@@ -120,6 +135,7 @@ template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_group
   if constexpr (OP == 1) return (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) ? BBDG_OPT_NG_TMEM
                                                                                      : BBDG_OPT_NG_SURF;  // OP_SURFACE
   if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
+  if constexpr (BBDG_OPT_TMEM && BBDG_OPT_TMEM64 && SZ == 8 && N >= BBDG_OPT_TMEM64_MIN_N) return BBDG_OPT_NG_TMEM8;
   return SZ == 4 ? g4[N] : g8[N];
 }
 
@@ -132,6 +148,10 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int KE = opt_ke<N, sz>();
   static constexpr int GW = 4, GT = 32 * GW;
   static constexpr bool VOL = OP != OP_SURFACE, SURF = OP != OP_VOLUME, RES = OP == OP_STAGE;
+  // fp64 stage: res is not staged (coalesced streaming loads in the epilogue instead), which
+  // frees the shared memory of two res tiles per group -> one more group at N = 6, 7, 9
+  static constexpr bool RESG = RES && sz == 8 && BBDG_OPT_RES_GLOBAL && N >= BBDG_OPT_RES_GLOBAL_MIN_N;
+  static constexpr bool RESS = RES && !RESG;   // res staged by TMA with the state
   static constexpr int PPW = 4 * KE / GW;   // faces per warp
   static_assert((4 * KE) % GW == 0, "faces must split evenly over the warps");
   static constexpr int NFS = odd_up(Nfp), NPS = odd_up(Np), NWS = Npm + 1;
@@ -140,7 +160,12 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   // slot counts (items per thread, rounded up); a slot is "full" if every thread has an item
   static constexpr int NS_ITEMS = PPW * Nfp;
   static constexpr int SS = SURF ? (NS_ITEMS + 31) / 32 : 0;
-  static constexpr bool TMH = BBDG_OPT_TMEM && sz == 4 && OP != OP_VOLUME && N >= BBDG_OPT_TMEM_MIN_N;
+  static constexpr bool TMH = BBDG_OPT_TMEM && OP != OP_VOLUME &&
+                              ((sz == 4 && N >= BBDG_OPT_TMEM_MIN_N) ||
+                               (sz == 8 && BBDG_OPT_TMEM64 && OP == OP_STAGE && N >= BBDG_OPT_TMEM64_MIN_N));
+  // per-point coefficient tables in TMEM too (fp32 only: they are stored as 32-bit words)
+  static constexpr bool TMC = TMH && sz == 4;
+  static constexpr int FW = sz / 4;   // 32-bit words per T (the V1/V2 scale factors stay exact)
   // L0 lane offsets hoisted (registers, or TMEM in TMEM mode) -- else one LDS.128 per item
   static constexpr bool HOIST_L0 = SS <= 2 || TMH;
   static constexpr int SV1 = VOL ? (KE * Npm + GT - 1) / GT : 0;
@@ -171,7 +196,7 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int S = rnd(NQ + 2 * A) + FSR;
   static constexpr int t_q = 0;                                   // [4][S] + shift slack
   static constexpr int t_res = rnd(t_q + 4 * S + 2 * A);          // same shape (RES)
-  static constexpr int t_geo = rnd(t_res + (RES ? 4 * S + 2 * A : 0));   // [KE][36]
+  static constexpr int t_geo = rnd(t_res + (RESS ? 4 * S + 2 * A : 0));   // [KE][36]
   static constexpr int t_nb = rnd(t_geo + KE * kGeoRec);          // [4][NB]
   static constexpr int t_bar = rnd(t_nb + (SURF ? 4 * NB : 0));   // mbarrier (8 bytes)
   static constexpr int stage_T = rnd(t_bar + 8 / sz + 1);
@@ -197,10 +222,11 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int C3W = (S3T + 1) / 2 > 0 ? (S3T + 1) / 2 : 1;
   static constexpr int H_SOF = 0, H_SEF = SSa_, H_SL0 = 2 * SSa_, H_C3 = H_SL0 + (HOIST_L0 ? 3 * SSa_ : 3);
   static constexpr int H_V1C = H_C3 + C3W, H_V1W = H_V1C + 2 * SV1a_, H_V1F = H_V1W + SV1a_;
-  static constexpr int H_V2P = H_V1F + SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
+  static constexpr int H_V2P = H_V1F + FW * SV1a_, H_V2G = H_V2P + 2 * SV2, H_V2M = H_V2G + 2 * SV2;
   static constexpr int H_V2F = H_V2M + SV2;
   // per-point coefficients (TMEM mode only): L0 4-vector + b! per S slot, gather 1/beta! 4-vector per V2 slot
-  static constexpr int H_L0C = H_V2F + SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_, NH = H_GF + 4 * SV2;
+  static constexpr int H_L0C = H_V2F + FW * SV2, H_FF = H_L0C + 4 * SSa_, H_GF = H_FF + SSa_;
+  static constexpr int NH = TMC ? H_GF + 4 * SV2 : H_L0C;
   static_assert(!TMH || NG * NH <= 512, "TMEM-parked tables exceed the 512 TMEM columns of an SM");
   static constexpr int tm_cols() {
     int c = 32;
@@ -328,6 +354,20 @@ template <int C> __device__ __forceinline__ void tm_ld(uint32_t ta, uint32_t* r)
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r[0]) : "r"(ta) : "memory");
   }
 }
+// a T as 32-bit TMEM words (doubles as two words, bit-exact)
+template <typename T> __device__ __forceinline__ void put_words(uint32_t* w, T v) {
+  if constexpr (sizeof(T) == 4) {
+    w[0] = __float_as_uint((float)v);
+  } else {
+    const unsigned long long b = (unsigned long long)__double_as_longlong((double)v);
+    w[0] = (uint32_t)b;
+    w[1] = (uint32_t)(b >> 32);
+  }
+}
+template <typename T> __device__ __forceinline__ T get_words(const uint32_t* w) {
+  if constexpr (sizeof(T) == 4) return (T)__uint_as_float(w[0]);
+  else return (T)__longlong_as_double((long long)(((unsigned long long)w[1] << 32) | w[0]));
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -335,8 +375,6 @@ __device__ __forceinline__ uint32_t lo16(uint32_t x) { return x & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t x) { return x >> 16; }
 __device__ __forceinline__ uint32_t pk(uint32_t a, uint32_t b) { return a | (b << 16); }
 
-// run f() for slot K of a phase with `count` items spread over `width` threads;
-// full slots are unguarded at compile time
 // value of item x (in slot x / 32, lane x % 32) of a level held one slot per register:
 // one shuffle per slot, the owning slot's result kept (all lanes must call it)
 template <int PS, typename T> __device__ __forceinline__ T warp_gather(const T* v, int x) {
@@ -349,6 +387,8 @@ template <int PS, typename T> __device__ __forceinline__ T warp_gather(const T* 
   return r;
 }
 
+// run f() for slot K of a phase with `count` items spread over `width` threads;
+// full slots are unguarded at compile time
 template <int K, int WIDTH, int COUNT, class F> __device__ __forceinline__ void slot(int idx, F&& f) {
   if constexpr ((K + 1) * WIDTH <= COUNT) {
     f();
@@ -526,7 +566,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_V1C + 2 * k] = v1c[k][0];
       hx[L::H_V1C + 2 * k + 1] = v1c[k][1];
       hx[L::H_V1W + k] = v1w[k];
-      hx[L::H_V1F + k] = __float_as_uint((float)v1f[k]);
+      put_words<T>(hx + L::H_V1F + L::FW * k, v1f[k]);
     }
 #pragma unroll
     for (int k = 0; k < SV2; ++k) {
@@ -535,10 +575,10 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_V2G + 2 * k] = v2g[k][0];
       hx[L::H_V2G + 2 * k + 1] = v2g[k][1];
       hx[L::H_V2M + k] = v2m[k];
-      hx[L::H_V2F + k] = __float_as_uint((float)v2f[k]);
+      put_words<T>(hx + L::H_V2F + L::FW * k, v2f[k]);
     }
 #pragma unroll
-    for (int k = 0; k < SS; ++k) {
+    for (int k = 0; k < (L::TMC ? SS : 0); ++k) {
       const int m = s_ef[k] & 0xff;
       const V4<T> c = l0c[m];
       hx[L::H_L0C + 4 * k] = __float_as_uint((float)c.x);
@@ -548,7 +588,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       hx[L::H_FF + k] = __float_as_uint((float)ffac[m]);
     }
 #pragma unroll
-    for (int k = 0; k < SV2; ++k) {
+    for (int k = 0; k < (L::TMC ? SV2 : 0); ++k) {
       const V4<T> gf = gfac[hi16(v2m[k]) & 1023];
       hx[L::H_GF + 4 * k] = __float_as_uint((float)gf.x);
       hx[L::H_GF + 4 * k + 1] = __float_as_uint((float)gf.y);
@@ -559,8 +599,8 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     tm_wait_st();
   }
   // per-point coefficients, from TMEM in TMEM mode (filled by the phase loads below)
-  V4<T> tl0[L::TMH ? SSa : 1], tgf[L::TMH ? SV2 : 1];
-  T tff[L::TMH ? SSa : 1];
+  V4<T> tl0[L::TMC ? SSa : 1], tgf[L::TMC ? SV2 : 1];
+  T tff[L::TMC ? SSa : 1];
   // reload one phase's tables from TMEM (no-op when they stay in registers)
   auto tm_load_s = [&] {
     if constexpr (L::TMH) {
@@ -569,10 +609,10 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
       uint32_t u[3 * SSa];
       if constexpr (L::HOIST_L0) tm_ld<3 * SSa>(ta + L::H_SL0, u);
       uint32_t cf[5 * SSa];
-      tm_ld<5 * SSa>(ta + L::H_L0C, cf);
+      if constexpr (L::TMC) tm_ld<5 * SSa>(ta + L::H_L0C, cf);
       tm_wait_ld();
 #pragma unroll
-      for (int k = 0; k < SS; ++k) {
+      for (int k = 0; k < (L::TMC ? SS : 0); ++k) {
         tl0[k] = V4<T>{(T)__uint_as_float(cf[4 * k]), (T)__uint_as_float(cf[4 * k + 1]),
                        (T)__uint_as_float(cf[4 * k + 2]), (T)__uint_as_float(cf[4 * k + 3])};
         tff[k] = (T)__uint_as_float(cf[4 * SSa + k]);
@@ -597,27 +637,27 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   };
   auto tm_load_v1 = [&] {
     if constexpr (L::TMH) {
-      uint32_t t[4 * SV1a];
-      tm_ld<4 * SV1a>(ta + L::H_V1C, t);
+      uint32_t t[(3 + L::FW) * SV1a];
+      tm_ld<(3 + L::FW) * SV1a>(ta + L::H_V1C, t);
       tm_wait_ld();
 #pragma unroll
       for (int k = 0; k < SV1; ++k) {
         v1c[k][0] = t[2 * k];
         v1c[k][1] = t[2 * k + 1];
         v1w[k] = t[2 * SV1a + k];
-        v1f[k] = (T)__uint_as_float(t[3 * SV1a + k]);
+        v1f[k] = get_words<T>(t + 3 * SV1a + L::FW * k);
       }
     }
   };
   auto tm_load_v2 = [&] {
     if constexpr (L::TMH) {
-      uint32_t t[6 * SV2];
-      tm_ld<6 * SV2>(ta + L::H_V2P, t);
+      uint32_t t[(5 + L::FW) * SV2];
+      tm_ld<(5 + L::FW) * SV2>(ta + L::H_V2P, t);
       uint32_t gq[4 * SV2];
-      tm_ld<4 * SV2>(ta + L::H_GF, gq);
+      if constexpr (L::TMC) tm_ld<4 * SV2>(ta + L::H_GF, gq);
       tm_wait_ld();
 #pragma unroll
-      for (int k = 0; k < SV2; ++k)
+      for (int k = 0; k < (L::TMC ? SV2 : 0); ++k)
         tgf[k] = V4<T>{(T)__uint_as_float(gq[4 * k]), (T)__uint_as_float(gq[4 * k + 1]),
                        (T)__uint_as_float(gq[4 * k + 2]), (T)__uint_as_float(gq[4 * k + 3])};
 #pragma unroll
@@ -627,7 +667,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         v2g[k][0] = t[2 * SV2 + 2 * k];
         v2g[k][1] = t[2 * SV2 + 2 * k + 1];
         v2m[k] = t[4 * SV2 + k];
-        v2f[k] = (T)__uint_as_float(t[5 * SV2 + k]);
+        v2f[k] = get_words<T>(t + 5 * SV2 + L::FW * k);
       }
     }
   };
@@ -647,7 +687,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   // (+ res) and the geometry records.  Field F's window is placed so that its data starts at
   // t_q + d0 + F S (d0 = (k0 Np) mod A); a window running past the array end leaves its last
   // sub-16-byte piece to plain loads, written before the barrier arrive (release).
-  constexpr int NCH = L::RES ? 9 : 5;
+  constexpr int NCH = L::RESS ? 9 : 5;
   auto issue_state = [&](int64_t k0, int nv, int st) {
     T* s = stage_ptr(st);
     uint64_t* bar = stage_bar(st);
@@ -772,7 +812,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const T u = bs * nb[0] - ab * loc[0];   // |Bs| jp
           const T jun = nf.x * (nb[1] - loc[1]) + nf.y * (nb[2] - loc[2]) + nf.z * (nb[3] - loc[3]);
           T fb;
-          if constexpr (L::TMH) fb = tff[k];
+          if constexpr (L::TMC) fb = tff[k];
           else fb = ffac[s_ef[k] & 0xff];
           sflux[fl] = fb * (tp * u - ab * jun);
           sflux[NB + fl] = fb * (cu * jun - u);
@@ -789,7 +829,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const int fl = hi16(s_of[k]), m = s_ef[k] & 0xff;
           const int ef = s_ef[k] >> 8;
           V4<T> c;
-          if constexpr (L::TMH) c = tl0[k];
+          if constexpr (L::TMC) c = tl0[k];
           else c = l0c[m];
           int o0, o1, o2, o3, o4, o5;
           if constexpr (L::HOIST_L0) {
@@ -917,7 +957,13 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         const T* gr = sgeo + e * kGeoRec;
         (void)gr;
         (void)a;
-        T r[4];
+        T r[4], rv[4];
+        if constexpr (L::RESG) {   // issued first: the loads overlap the smem work below
+          if (KE == 1 || (int)(hi16(v2m[k]) >> 10) < nv) {
+#pragma unroll
+            for (int F = 0; F < 4; ++F) rv[F] = __ldcs(resF + F * fs + t);
+          }
+        }
         if constexpr (L::VOL) {
           const int p0 = lo16(v2p[k][0]), p1 = hi16(v2p[k][0]), p2 = lo16(v2p[k][1]), p3 = hi16(v2p[k][1]);
           if constexpr (L::WAOS) {
@@ -937,7 +983,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
         if constexpr (L::SURF) {
           const int g0 = lo16(v2g[k][0]), g1 = hi16(v2g[k][0]), g2 = lo16(v2g[k][1]), g3 = hi16(v2g[k][1]);
           V4<T> gf;
-          if constexpr (L::TMH) gf = tgf[k];
+          if constexpr (L::TMC) gf = tgf[k];
           else gf = gfac[a];
           const P2<T>* W2 = reinterpret_cast<const P2<T>*>(sW);
           const P2<T> w0 = W2[g0], w1 = W2[g1], w2 = W2[g2], w3 = W2[g3];
@@ -969,7 +1015,9 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
             // res = A res + dt rhs; q_out = q_in + B res   (reference solver.py:211-213)
 #pragma unroll
             for (int F = 0; F < 4; ++F) {
-              T x = sq[L::RQ + F * S + t] * p.rk_a;
+              T x;
+              if constexpr (L::RESG) x = rv[F] * p.rk_a;
+              else x = sq[L::RQ + F * S + t] * p.rk_a;
               x = x + p.dt * r[F];
               const T qn = sq[F * S + t] + p.rk_b * x;
               st_stream(resF + F * fs + t, x);

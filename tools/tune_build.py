@@ -5,14 +5,10 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"s1d", "s2d", "s4d"}
+F64 = {"b0d", "t0d"}
 VARIANTS = {
-    "s1": ["-DBBDG_OPT_SHF_SLOTS=1"],
-    "s2": ["-DBBDG_OPT_SHF_SLOTS=2"],
-    "s4": ["-DBBDG_OPT_SHF_SLOTS=4"],
-    "s2d": ["-DBBDG_OPT_SHF_SLOTS=2"],
-    "s1d": ["-DBBDG_OPT_SHF_SLOTS=1"],
-    "s4d": ["-DBBDG_OPT_SHF_SLOTS=4"],
+    "b0d": ["-DBBDG_OPT_RES_GLOBAL=0", "-DBBDG_OPT_TMEM64=0"],   # fp64 before res-from-HBM / TMEM tables
+    "t0d": ["-DBBDG_OPT_TMEM64=0"],                               # res from HBM only
 }
 
 if __name__ == "__main__":

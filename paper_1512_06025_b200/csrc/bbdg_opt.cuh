@@ -110,17 +110,24 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_shf_slots() {
 #ifndef BBDG_OPT_NG_TMEM
 #define BBDG_OPT_NG_TMEM 5   // groups of the fused fp32 kernels whose hoisted tables live in TMEM
 #endif
-#ifndef BBDG_OPT_RES_GLOBAL
-#define BBDG_OPT_RES_GLOBAL 1   // fp64 stage: the LSRK register is read straight from HBM in the epilogue
+// per order: the stage reads the LSRK register straight from HBM in the epilogue instead of
+// staging it (frees shared memory for more groups where shared memory caps them)
+#ifndef BBDG_OPT_RESG4
+#define BBDG_OPT_RESG4 0, 0, 0, 0, 0, 0, 0, 0, 0, 0
 #endif
-#ifndef BBDG_OPT_RES_GLOBAL_MIN_N
-#define BBDG_OPT_RES_GLOBAL_MIN_N 3   // (measured: N = 1, 2 lose 3-9 %; they are not smem-bound)
+#ifndef BBDG_OPT_RESG8
+#define BBDG_OPT_RESG8 0, 0, 0, 1, 1, 1, 1, 1, 1, 1   // (measured: N = 1, 2 lose 3-9 %; not smem-bound)
 #endif
+template <int N, int SZ> __host__ __device__ constexpr bool opt_res_global() {
+  constexpr int r4[10] = {BBDG_OPT_RESG4};
+  constexpr int r8[10] = {BBDG_OPT_RESG8};
+  return (SZ == 4 ? r4[N] : r8[N]) != 0;
+}
 #ifndef BBDG_OPT_TMEM64
 #define BBDG_OPT_TMEM64 1   // fp64 fused kernels park their offset tables in TMEM too (coefficients stay in smem)
 #endif
-#ifndef BBDG_OPT_NG_TMEM8
-#define BBDG_OPT_NG_TMEM8 4
+#ifndef BBDG_OPT_NGT8
+#define BBDG_OPT_NGT8 0, 4, 4, 4, 4, 5, 4, 4, 4, 4   // fp64 TMEM-mode groups (measured: 5 wins at N=5 only)
 #endif
 #ifndef BBDG_OPT_TMEM64_MIN_N
 #define BBDG_OPT_TMEM64_MIN_N 4
@@ -135,7 +142,8 @@ template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_group
   if constexpr (OP == 1) return (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) ? BBDG_OPT_NG_TMEM
                                                                                      : BBDG_OPT_NG_SURF;  // OP_SURFACE
   if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
-  if constexpr (BBDG_OPT_TMEM && BBDG_OPT_TMEM64 && SZ == 8 && N >= BBDG_OPT_TMEM64_MIN_N) return BBDG_OPT_NG_TMEM8;
+  constexpr int gt8[10] = {BBDG_OPT_NGT8};
+  if constexpr (BBDG_OPT_TMEM && BBDG_OPT_TMEM64 && SZ == 8 && N >= BBDG_OPT_TMEM64_MIN_N) return gt8[N];
   return SZ == 4 ? g4[N] : g8[N];
 }
 
@@ -148,9 +156,9 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int KE = opt_ke<N, sz>();
   static constexpr int GW = 4, GT = 32 * GW;
   static constexpr bool VOL = OP != OP_SURFACE, SURF = OP != OP_VOLUME, RES = OP == OP_STAGE;
-  // fp64 stage: res is not staged (coalesced streaming loads in the epilogue instead), which
-  // frees the shared memory of two res tiles per group -> one more group at N = 6, 7, 9
-  static constexpr bool RESG = RES && sz == 8 && BBDG_OPT_RES_GLOBAL && N >= BBDG_OPT_RES_GLOBAL_MIN_N;
+  // res not staged (coalesced streaming loads in the epilogue instead): frees the shared
+  // memory of two res tiles per group (fp64: one more group at N = 6, 7, 9)
+  static constexpr bool RESG = RES && opt_res_global<N, sz>();
   static constexpr bool RESS = RES && !RESG;   // res staged by TMA with the state
   static constexpr int PPW = 4 * KE / GW;   // faces per warp
   static_assert((4 * KE) % GW == 0, "faces must split evenly over the warps");

@@ -5,10 +5,10 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"b0d", "t0d"}
+F64 = {"n5d"}
 VARIANTS = {
-    "b0d": ["-DBBDG_OPT_RES_GLOBAL=0", "-DBBDG_OPT_TMEM64=0"],   # fp64 before res-from-HBM / TMEM tables
-    "t0d": ["-DBBDG_OPT_TMEM64=0"],                               # res from HBM only
+    "n5d": ["-DBBDG_OPT_NG_TMEM8=5"],
+    "j6": ["-DBBDG_OPT_NG_TMEM=6"],
 }
 
 if __name__ == "__main__":

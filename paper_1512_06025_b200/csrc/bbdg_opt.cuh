@@ -71,7 +71,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define BBDG_OPT_KE4 0, 32, 24, 12, 6, 4, 3, 2, 2, 1
 #endif
 #ifndef BBDG_OPT_KE8
-#define BBDG_OPT_KE8 0, 16, 12, 6, 4, 2, 3, 2, 1, 1
+#define BBDG_OPT_KE8 0, 16, 12, 6, 4, 2, 2, 2, 1, 1   // (N=6: KE 2 -> 4 groups, +7 % with res from HBM)
 #endif
 #ifndef BBDG_OPT_NG4
 #define BBDG_OPT_NG4 0, 4, 4, 4, 4, 4, 4, 4, 3, 4

@@ -337,7 +337,8 @@ def run_ours(args, rank, world):
     out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                   "h2d_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
                   "d2h_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
-                  "what": ("lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H"
+                  "what": ("lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H "
+                           "(chunk-pipelined through bbdg_step_host for states >= 32 MB: copies overlap stages)"
                            if world == 1 else "per rank: pinned host slab H2D + DistWaveSystem.step_into (5 "
                            "exchanged stages) + D2H, max over ranks")}
     if world == 1 and args.nodal and not args.quick:

@@ -127,10 +127,10 @@ template <int N, int SZ> __host__ __device__ constexpr bool opt_res_global() {
 #define BBDG_OPT_TMEM64 1   // fp64 fused kernels park their offset tables in TMEM too (coefficients stay in smem)
 #endif
 #ifndef BBDG_OPT_NGT8
-#define BBDG_OPT_NGT8 0, 4, 4, 4, 4, 5, 4, 4, 4, 4   // fp64 TMEM-mode groups (measured: 5 wins at N=5 only)
+#define BBDG_OPT_NGT8 0, 4, 4, 5, 4, 5, 4, 4, 4, 4   // fp64 TMEM-mode groups (measured: 5 win at N=3, 5)
 #endif
 #ifndef BBDG_OPT_TMEM64_MIN_N
-#define BBDG_OPT_TMEM64_MIN_N 4
+#define BBDG_OPT_TMEM64_MIN_N 3
 #endif
 #ifndef BBDG_OPT_TMEM_MIN_N
 #define BBDG_OPT_TMEM_MIN_N 4   // (measured: no gain below N = 4, where registers do not bind)

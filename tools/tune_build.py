@@ -5,10 +5,10 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"m3d", "m4d"}
+F64 = set()
 VARIANTS = {
-    "m3d": ["-DBBDG_OPT_TMEM64_MIN_N=3", "-DBBDG_OPT_NGT8=0,4,4,5,5,5,4,4,4,4"],   # fp64 N=3, 4: 5 TMEM groups
-    "m4d": ["-DBBDG_OPT_NGT8=0,4,4,4,5,5,4,4,4,4"],                              # fp64 N=4: 5 groups
+    "k2": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,2,2,1"],   # fp32 N=2: KE 16
+    "k3": ["-DBBDG_OPT_KE4=0,32,24,8,6,4,3,2,2,1"],    # fp32 N=3: KE 8
 }
 
 if __name__ == "__main__":

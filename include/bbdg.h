@@ -6,7 +6,9 @@
  * DEVICE pointers to C-contiguous (4, K, Np) arrays of the context's dtype
  * (reference FieldState.q layout, solver.py:80-93); `stream` is a
  * cudaStream_t (NULL = legacy default stream).  No call allocates device
- * memory on the hot path and no call synchronises the device.  Every function
+ * memory on the hot path and no call synchronises the device.  State pointers must be 16-byte
+ * aligned (the fused kernels stage field planes with TMA bulk copies; every cudaMalloc'd or
+ * torch-allocated buffer is); misaligned pointers return BBDG_ERR_ARG.  Every function
  * returns a bbdg_status; bbdg_last_error() holds a message for the calling
  * thread.  Results are deterministic (owner-computes, no atomics).
  */
@@ -28,11 +30,16 @@ typedef enum {
 
 enum { BBDG_BASIS_BERNSTEIN = 0, BBDG_BASIS_NODAL = 1 };
 enum { BBDG_F32 = 0, BBDG_F64 = 1 };
-/* lift modes of BernsteinRefOps.lift_flux (bernstein.py:457-466).  The nodal basis runs the
- * reference's dense path (nodal.py:236-241) either as node-per-thread kernels (DENSE, paper
- * "NPT") or as block-partitioned tensor-core GEMMs with a fused chain-rule/lift epilogue
- * (BLOCKED, paper "EPT": fp64 DMMA, fp32 3xTF32); BLOCKED is nodal-only. */
-enum { BBDG_LIFT_FACTORIZED = 0, BBDG_LIFT_OPTIMAL = 1, BBDG_LIFT_DENSE = 2, BBDG_LIFT_BLOCKED = 3 };
+/* lift modes of BernsteinRefOps.lift_flux (bernstein.py:457-466).  FACTORIZED (the reference
+ * default, L = E_L L0, bernstein.py:301-310) and OPTIMAL (Alg. 1, :313-329) both run as L0 plus
+ * the one-degree reduction sweeps in shared memory (E_L is their composition; the reference's
+ * own two modes differ by <= 2.4e-16).  ELL applies E_L as stored fixed-width rows (the paper's
+ * non-optimal Alg. 3 surface kernel, kept for comparison).  The nodal basis runs the reference's
+ * dense path (nodal.py:236-241) either as node-per-thread kernels (DENSE, paper "NPT") or as
+ * block-partitioned tensor-core GEMMs with a fused chain-rule/lift epilogue (BLOCKED, paper
+ * "EPT": fp64 DMMA, fp32 3xTF32); BLOCKED is nodal-only. */
+enum { BBDG_LIFT_FACTORIZED = 0, BBDG_LIFT_OPTIMAL = 1, BBDG_LIFT_DENSE = 2, BBDG_LIFT_BLOCKED = 3,
+       BBDG_LIFT_ELL = 4 };
 
 typedef struct bbdg_ctx bbdg_ctx;
 
@@ -98,9 +105,14 @@ int bbdg_lsrk_update(int dtype, int64_t n, void* q, void* res, const void* rhs, 
                      double dt, void* stream);
 
 /* lsrk4_step (solver.py:196-214) with the reference's in-place semantics:
- * zeroes res, runs the five fused stages ping-ponging q <-> q_tmp and leaves
- * the result in q.  q_tmp and res are caller-owned (4,K,Np) scratch. */
+ * zeroes res, runs the five fused stages and leaves the result in q.  q_tmp,
+ * q_tmp2 and res are caller-owned (4,K,Np) scratch.  With q_tmp2 the stages run
+ * q -> q_tmp -> q_tmp2 -> q_tmp -> q_tmp2 -> q (the last stage writes q); with
+ * q_tmp2 == NULL (and in bbdg_step) they alternate q <-> q_tmp and one device
+ * copy returns the result to q. */
 int bbdg_step(bbdg_ctx* ctx, void* q, void* q_tmp, void* res, double dt, int lift_mode, void* stream);
+int bbdg_step2(bbdg_ctx* ctx, void* q, void* q_tmp, void* q_tmp2, void* res, double dt, int lift_mode,
+               void* stream);
 
 /* lsrk4_step on a host state (solver.py:196-214 called with a numpy q): H2D of
  * host_q, the five stages and the D2H of the result into host_q, pipelined over
@@ -138,6 +150,18 @@ int bbdg_error_l2(int dtype, int64_t K, int Np, int nq, const void* q0, const do
  * nodal_to_bernstein's matrix for the Bernstein basis and the identity for nodal. */
 int bbdg_project_standing_wave(int dtype, int64_t K, int Np, const double* tmat, const double* lam,
                                const double* verts, double tau, void* q, void* stream);
+
+/* Operator-level applies of the reference ops bundle (no mesh; degrees 1..20; device arrays,
+ * C-contiguous, batch-major):
+ *   bbdg_ops_grad: BernsteinRefOps.grad (bernstein.py:436-444), q (nb, Np) -> dr, ds, dt (nb, Np)
+ *   bbdg_ops_lift: lift_apply_factorized / lift_apply_optimal (bernstein.py:301-329),
+ *                  flux (nb, 4, Nfp) -> out (nb, Np), as L0 + one-degree reduction sweeps
+ *   bbdg_dense_apply: opcount.dense_apply (opcount.py:38-43), y (nb, nrows) = x (nb, ncols) A^T
+ *                  with A (nrows, ncols) row-major (dense lift, nodal grad) */
+int bbdg_ops_grad(int N, int dtype, int64_t nb, const void* q, void* dr, void* ds, void* dt, void* stream);
+int bbdg_ops_lift(int N, int dtype, int64_t nb, const void* flux, void* out, void* stream);
+int bbdg_dense_apply(int dtype, int64_t nb, int nrows, int ncols, const void* A, const void* x, void* y,
+                     void* stream);
 
 /* Introspection used by tests and the benchmark. */
 int bbdg_tile_elems(int N, int dtype);

@@ -230,38 +230,54 @@ class NodalTables:
 
 
 # ----------------------------------------------------------------- trace maps (mesh.py:158-188)
-def trace_maps(vertices, tets, etoe, etof, face_pts, trace, Np, h_elem):
-    """Coordinate-matched flat gather (K,4,Nfp) + boundary mask (vectorised)."""
+def trace_maps(vertices, tets, etoe, etof, face_pts, trace, Np, h_elem, rows=None):
+    """Coordinate-matched flat gather (K,4,Nfp) + boundary mask (vectorised, bounded chunks).
+
+    ``rows``: optional list of element ranges (k0, k1); only their gather rows are built (the
+    others stay -1), for spot checks of meshes too large for the full map."""
     K, Nfp = len(tets), face_pts.shape[1]
     lam = np.stack([-(1.0 + face_pts[..., 0] + face_pts[..., 1] + face_pts[..., 2]) / 2.0,
                     (1.0 + face_pts[..., 0]) / 2.0, (1.0 + face_pts[..., 1]) / 2.0,
                     (1.0 + face_pts[..., 2]) / 2.0], -1)                    # (4,Nfp,4)
-    V = vertices[tets]                                                     # (K,4,3)
-    phys = np.einsum("fnl,klx->kfnx", lam, V)                              # (K,4,Nfp,3)
+
+    def phys(ks):                                                          # (..., 4, Nfp, 3)
+        return np.einsum("fnl,...lx->...fnx", lam, vertices[tets[ks]])
+
     kk = np.arange(K)[:, None]
     bnd = (etoe == kk) & (etof == np.arange(4)[None, :])
-    mine = phys                                                             # (K,4,Nfp,3)
-    theirs = phys[etoe, etof]                                               # (K,4,Nfp,3)
-    d = np.linalg.norm(mine[:, :, :, None, :] - theirs[:, :, None, :, :], axis=-1)
-    perm = np.argmin(d, axis=-1)                                            # (K,4,Nfp)
+    gather = np.full((K, 4, Nfp), -1, dtype=np.int64)
     tol = 1e-8 * np.maximum(h_elem, 1.0)
-    dmin = np.take_along_axis(d, perm[..., None], -1)[..., 0]
-    if np.any((dmin.max(axis=2) > tol[:, None]) & ~bnd):
-        raise ValueError("non-conforming mesh")
-    gather = etoe[..., None] * Np + trace[etof][np.arange(K)[:, None, None], np.arange(4)[None, :, None], perm]
-    own = kk[:, :, None] * Np + trace[None, :, :]
-    return np.where(bnd[..., None], own, gather), bnd
+    step = max(1, (1 << 22) // (4 * Nfp * Nfp))                             # bounded (n,4,Nfp,Nfp) chunks
+    for r0, r1 in (rows if rows is not None else [(0, K)]):
+        for k0 in range(r0, r1, step):
+            k1 = min(r1, k0 + step)
+            mine = phys(np.arange(k0, k1))                                  # (n,4,Nfp,3)
+            theirs = np.einsum("kfnl,kflx->kfnx", lam[etof[k0:k1]], vertices[tets[etoe[k0:k1]]])
+            d = np.linalg.norm(mine[:, :, :, None, :] - theirs[:, :, None, :, :], axis=-1)
+            perm = np.argmin(d, axis=-1)                                    # (n,4,Nfp)
+            dmin = np.take_along_axis(d, perm[..., None], -1)[..., 0]
+            b = bnd[k0:k1]
+            if np.any((dmin.max(axis=2) > tol[k0:k1, None]) & ~b):
+                raise ValueError("non-conforming mesh")
+            ef = etof[k0:k1]
+            g = etoe[k0:k1, :, None] * Np + trace[ef][np.arange(k1 - k0)[:, None, None], np.arange(4)[None, :, None],
+                                                      perm]
+            own = np.arange(k0, k1)[:, None, None] * Np + trace[None, :, :]
+            gather[k0:k1] = np.where(b[..., None], own, g)
+    return gather, bnd
 
 
 # ----------------------------------------------------------------- the solver (solver.py:99-214)
 class OracleSystem:
-    def __init__(self, mesh_arrays: dict, tables, kappa, rho, dtype=np.float64):
+    def __init__(self, mesh_arrays: dict, tables, kappa, rho, dtype=np.float64, rows=None, maps=None):
         m = mesh_arrays
         self.t = tables
         self.dtype = np.dtype(dtype).type
         self.K = len(m["tets"])
-        self.gather, self.boundary = trace_maps(m["vertices"], m["tets"], m["etoe"], m["etof"], tables.face_pts,
-                                                tables.trace, tables.Np, m["h_elem"])
+        if maps is None:
+            maps = trace_maps(m["vertices"], m["tets"], m["etoe"], m["etof"], tables.face_pts, tables.trace,
+                              tables.Np, m["h_elem"], rows)
+        self.gather, self.boundary = maps
         rc = rho * np.sqrt(kappa / rho)
         mean_rc = 0.5 * (rc[:, None] + rc[m["etoe"]])
         d = self.dtype
@@ -273,37 +289,59 @@ class OracleSystem:
         self.kappa = kappa.astype(d)[:, None]
         self.inv_rho = (1.0 / rho).astype(d)[:, None]
 
-    def volume_rhs(self, q):
-        dq = np.empty_like(q)
-        B = self.rst_dx
-        gr, gs, gt = (g.reshape(q.shape) for g in self.t.grad(q.reshape(4 * self.K, -1)))
+    # `sl` (a slice of elements) evaluates the rows of those elements only -- the same arithmetic per
+    # element, so config-2 / bench-size meshes are checked in bounded-memory chunks (rhs_chunked)
+    def volume_rhs(self, q, sl=slice(None)):
+        qs = q[:, sl]
+        dq = np.empty_like(qs)
+        B = self.rst_dx[sl]
+        gr, gs, gt = (g.reshape(qs.shape) for g in self.t.grad(qs.reshape(4 * qs.shape[1], -1)))
         for i in range(3):
-            dq[1 + i] = -self.inv_rho * (B[:, 0, i, None] * gr[0] + B[:, 1, i, None] * gs[0] + B[:, 2, i, None] * gt[0])
+            dq[1 + i] = -self.inv_rho[sl] * (B[:, 0, i, None] * gr[0] + B[:, 1, i, None] * gs[0]
+                                             + B[:, 2, i, None] * gt[0])
         div = sum(B[:, 0, i, None] * gr[1 + i] + B[:, 1, i, None] * gs[1 + i] + B[:, 2, i, None] * gt[1 + i]
                   for i in range(3))
-        dq[0] = -self.kappa * div
+        dq[0] = -self.kappa[sl] * div
         return dq
 
-    def surface_rhs(self, q, lift_mode="factorized"):
-        loc = q[..., self.t.trace]
-        nbr = q.reshape(4, -1)[:, self.gather]
+    def surface_rhs(self, q, lift_mode="factorized", sl=slice(None)):
+        loc = q[:, sl][..., self.t.trace]
+        nbr = q.reshape(4, -1)[:, self.gather[sl]]
         jump = nbr - loc
-        jp = np.where(self.boundary[:, :, None], -2.0 * loc[0], jump[0])
-        n = self.normals
+        jp = np.where(self.boundary[sl][:, :, None], -2.0 * loc[0], jump[0])
+        n = self.normals[sl]
         jun = n[:, :, 0, None] * jump[1] + n[:, :, 1, None] * jump[2] + n[:, :, 2, None] * jump[3]
         half = q.dtype.type(0.5)
-        Fp = half * (self.tau_p * jp - jun) * self.face_scale
-        Fu = half * (self.tau_u * jun - jp) * self.face_scale
+        Fp = half * (self.tau_p[sl] * jp - jun) * self.face_scale[sl]
+        Fu = half * (self.tau_u[sl] * jun - jp) * self.face_scale[sl]
         flux = np.stack([Fp] + [n[:, :, i, None] * Fu for i in range(3)])
         lifted = self.t.lift(flux, lift_mode, q.dtype)
-        dq = np.empty_like(q)
-        dq[0] = self.kappa * lifted[0]
+        dq = np.empty((4,) + lifted.shape[1:], dtype=q.dtype)
+        dq[0] = self.kappa[sl] * lifted[0]
         for i in range(3):
-            dq[1 + i] = self.inv_rho * lifted[1 + i]
+            dq[1 + i] = self.inv_rho[sl] * lifted[1 + i]
         return dq
 
-    def rhs(self, q, lift_mode="factorized"):
-        return self.volume_rhs(q) + self.surface_rhs(q, lift_mode)
+    def rhs(self, q, lift_mode="factorized", sl=slice(None)):
+        return self.volume_rhs(q, sl) + self.surface_rhs(q, lift_mode, sl)
+
+    def rhs_chunked(self, q, lift_mode="factorized", k0=0, k1=None, chunk=2048):
+        """rhs rows of elements [k0, k1) (all of them by default), evaluated chunk by chunk."""
+        k1 = self.K if k1 is None else k1
+        out = np.empty((4, k1 - k0, q.shape[2]), dtype=q.dtype)
+        for a in range(k0, k1, chunk):
+            b = min(k1, a + chunk)
+            out[:, a - k0 : b - k0] = self.rhs(q, lift_mode, slice(a, b))
+        return out
+
+    def stage(self, q, res, rk_a, rk_b, dt, lift_mode="factorized", k0=0, k1=None, chunk=2048):
+        """One LSRK stage for elements [k0, k1): (q_out, res_out) rows (solver.py:208-213)."""
+        k1 = self.K if k1 is None else k1
+        t = q.dtype.type
+        k = self.rhs_chunked(q, lift_mode, k0, k1, chunk)
+        r = res[:, k0:k1] * t(rk_a)
+        r += t(dt) * k
+        return q[:, k0:k1] + t(rk_b) * r, r
 
     def lsrk4_step(self, q, dt, lift_mode="factorized", res=None):
         if res is None:

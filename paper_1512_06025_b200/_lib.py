@@ -14,7 +14,9 @@ LIB_PATH = Path(os.environ.get("BBDG_LIB") or Path(__file__).resolve().parent / 
 
 BASIS = {"bernstein": 0, "nodal": 1}
 DTYPE = {"float32": 0, "float64": 1}
-LIFT = {"factorized": 0, "optimal": 1, "dense": 2, "blocked": 3}   # blocked: nodal tensor-core path
+LIFT = {"factorized": 0, "optimal": 1, "dense": 2, "blocked": 3, "ell": 4}
+# factorized and optimal both run the L0 + reduction-sweep kernels; "ell" is the paper's Alg. 3
+# E_L-rows kernel; "blocked" is the nodal tensor-core path
 OP = {"volume": 0, "surface": 1, "rhs": 2, "stage": 3}
 
 _P = C.c_void_p
@@ -40,11 +42,15 @@ SIGNATURES = [
     ("bbdg_rhs_range", C.c_int, [_P, _P, _P, C.c_int, _I64, _I64, _P]),
     ("bbdg_lsrk_update", C.c_int, [C.c_int, _I64, _P, _P, _P, _D, _D, _D, _P]),
     ("bbdg_step", C.c_int, [_P, _P, _P, _P, _D, C.c_int, _P]),
+    ("bbdg_step2", C.c_int, [_P, _P, _P, _P, _P, _D, C.c_int, _P]),
     ("bbdg_step_host", C.c_int, [_P, _P, _P, _P, _P, _D, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P]),
     ("bbdg_halo_pack", C.c_int, [_P, _P, _P, _P, _I64, _P]),
     ("bbdg_energy", C.c_int, [C.c_int, _I64, C.c_int, _P, _P, _P, _P, _P, _P]),
     ("bbdg_error_l2", C.c_int, [C.c_int, _I64, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),
     ("bbdg_project_standing_wave", C.c_int, [C.c_int, _I64, C.c_int, _P, _P, _P, _D, _P, _P]),
+    ("bbdg_ops_grad", C.c_int, [C.c_int, C.c_int, _I64, _P, _P, _P, _P, _P]),
+    ("bbdg_ops_lift", C.c_int, [C.c_int, C.c_int, _I64, _P, _P, _P]),
+    ("bbdg_dense_apply", C.c_int, [C.c_int, _I64, C.c_int, C.c_int, _P, _P, _P, _P]),
     ("bbdg_tile_elems", C.c_int, [C.c_int, C.c_int]),
     ("bbdg_kernel_smem", C.c_int64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
 ]

@@ -30,6 +30,8 @@ from functools import lru_cache
 
 import numpy as np
 
+from . import _device, _lib
+from .modal import tet_rule, triangle_rule
 from .multiindex import (
     TET_VERTICES,
     barycentric_from_rst,
@@ -42,7 +44,9 @@ from .multiindex import (
     simplex_dim,
     simplex_indices,
     tet_dim,
+    tri_barycentric_from_rs,
 )
+from .sparse import SparseRowOperator, from_dense
 
 REF_MEASURE = {1: 2.0, 2: 2.0, 3: 4.0 / 3.0}
 
@@ -192,6 +196,124 @@ def derivative_tables(N: int):
     return idx.astype(float), cols
 
 
+def basis_dlambda_matrix(N: int, d: int, bary, i: int) -> np.ndarray:
+    """Formal d/d lambda_i of every degree-N basis function at (npts, d+1) points
+    (reference bernstein.py:98-112): C(N,alpha) alpha_i lambda^(alpha - e_i)."""
+    bary = np.atleast_2d(np.asarray(bary, dtype=float))
+    idx = simplex_indices(N, d)
+    out = np.zeros((bary.shape[0], len(idx)))
+    for p, alpha in enumerate(idx):
+        if alpha[i] == 0:
+            continue
+        col = float(_multinomial(N, alpha)) * alpha[i] * np.ones(bary.shape[0])
+        for m, a in enumerate(alpha):
+            aa = a - 1 if m == i else a
+            if aa:
+                col *= bary[:, m] ** aa
+        out[:, p] = col
+    return out
+
+
+def face_mass_matrix(N: int) -> np.ndarray:
+    return mass_matrix(N, 2)
+
+
+@dataclass(frozen=True, eq=False)
+class BernsteinDerivativeSet:
+    """D^0..D^3 as fixed-width rows (reference bernstein.py:182-197): row alpha of D^i holds
+    alpha_j at column alpha + e_i - e_j; one (Np, 4) value table backs all four."""
+
+    N: int
+    values: np.ndarray
+    ops: tuple
+
+    def apply_all(self, q):
+        return tuple(op.apply(q) for op in self.ops)
+
+
+@lru_cache(maxsize=None)
+def derivative_ops(N: int) -> BernsteinDerivativeSet:
+    values, cols = derivative_tables(N)
+    Np = tet_dim(N)
+    ops = tuple(SparseRowOperator(Np, Np, values, cols[i].astype(np.intp)) for i in range(4))
+    return BernsteinDerivativeSet(N=N, values=values, ops=ops)
+
+
+@lru_cache(maxsize=None)
+def build_L0(N: int) -> SparseRowOperator:
+    """L0 = (N+1)^2/2 E^T E from its closed form (reference bernstein.py:221-229); <= 7 per row."""
+    return from_dense(L0_dense(N))
+
+
+@dataclass(frozen=True, eq=False)
+class LiftFactorization:
+    """Face lift without the dense matrix (reference bernstein.py:239-270)."""
+
+    N: int
+    Nfp: int
+    L0: SparseRowOperator
+    EL: SparseRowOperator     # (Np, 4 Nfp), <= Nfp + 3 entries per row
+    ell: np.ndarray           # (N+1,), ell[0] = 1
+    reductions: tuple         # (E^m_{m-1})^T for m = N..1, <= 3 per row
+    layers: tuple             # FaceLayers per face
+
+    def astype(self, dtype) -> "LiftFactorization":
+        return LiftFactorization(self.N, self.Nfp, self.L0.astype(dtype), self.EL.astype(dtype),
+                                 self.ell.astype(dtype), tuple(r.astype(dtype) for r in self.reductions),
+                                 self.layers)
+
+
+@lru_cache(maxsize=None)
+def build_lift(N: int) -> LiftFactorization:
+    """Reference bernstein.py:273-298, from the closed forms (E_L, L0, one-degree reductions)."""
+    reductions = tuple(from_dense(elevation_dense(m, 2).T) for m in range(N, 0, -1))
+    return LiftFactorization(N=N, Nfp=face_dim(N), L0=build_L0(N), EL=from_dense(el_dense(N)),
+                             ell=lift_scalings(N), reductions=reductions,
+                             layers=tuple(face_layers(N, f) for f in range(4)))
+
+
+def _lift_device(N: int, flux):
+    """bbdg_ops_lift: (..., 4, Nfp) -> (..., Np), L0 + one-degree reduction sweeps on the device."""
+    fd, host = _device.to_device(flux)
+    Nfp = face_dim(N)
+    if tuple(fd.shape[-2:]) != (4, Nfp):
+        raise ValueError(f"flux must end in (4, {Nfp}), got {tuple(fd.shape[-2:])}")
+    out = _device.torch().empty(tuple(fd.shape[:-2]) + (tet_dim(N),), dtype=fd.dtype, device=fd.device)
+    nb = fd.numel() // (4 * Nfp)
+    _lib.check(_lib.load().bbdg_ops_lift(N, _device.dtype_id(fd), nb, fd.data_ptr(), out.data_ptr(),
+                                         _device.stream()), "bbdg_ops_lift")
+    return _device.back(out, host)
+
+
+def lift_apply_factorized(lf: LiftFactorization, flux):
+    """sum_f L^f flux_f with L = E_L L0 (reference bernstein.py:301-310).  E_L is the composition of
+    the one-degree reductions scaled by ell_j, so the device applies it as those sweeps; the result
+    equals the reference's E_L row product to rounding (the reference's own modes differ by <= 2.4e-16)."""
+    if tuple(np.shape(flux))[-2:] != (4, lf.Nfp):
+        raise ValueError(f"flux must end in (4, {lf.Nfp}), got {tuple(np.shape(flux))[-2:]}")
+    return _lift_device(lf.N, flux)
+
+
+def lift_apply_optimal(lf: LiftFactorization, flux):
+    """Slice-by-slice lift, Algorithm 1 (reference bernstein.py:313-329): L0 per face, then N
+    cascaded one-degree reductions writing layer j scaled by ell_j -- on the device."""
+    if tuple(np.shape(flux))[-2:] != (4, lf.Nfp):
+        raise ValueError(f"flux must end in (4, {lf.Nfp}), got {tuple(np.shape(flux))[-2:]}")
+    return _lift_device(lf.N, flux)
+
+
+def dense_lift_oracle(N: int, f: int) -> np.ndarray:
+    """Quadrature-assembled M^{-1} M^f for one face (reference bernstein.py:350-365; a host-side
+    check of the closed-form lifts, not used by any kernel)."""
+    pts3, w3 = tet_rule(2 * N + 1)
+    B3 = basis_matrix(N, 3, barycentric_from_rst(pts3))
+    M = B3.T @ (w3[:, None] * B3)
+    pts2, w2 = triangle_rule(2 * N + 2)
+    bary2 = tri_barycentric_from_rs(pts2)
+    C = basis_matrix(N, 3, np.insert(bary2, f, 0.0, axis=1)).T @ (w2[:, None] * basis_matrix(N, 2, bary2))
+    return np.linalg.solve(M, C)
+
+
 @dataclass(frozen=True, eq=False)
 class BernsteinRefOps:
     """Degree-N Bernstein bundle (duck type of reference bernstein.py:387-466).
@@ -232,6 +354,41 @@ class BernsteinRefOps:
     @property
     def ell(self) -> np.ndarray:
         return lift_scalings(self.N)
+
+    @property
+    def derivs(self) -> BernsteinDerivativeSet:
+        return derivative_ops(self.N)
+
+    @property
+    def lift(self) -> LiftFactorization:
+        return build_lift(self.N)
+
+    def grad(self, q):
+        """Reference-coordinate derivatives (bernstein.py:436-444) on the device:
+        (d/dr, d/ds, d/dt) = ((D^1 - D^0) q, (D^2 - D^0) q, (D^3 - D^0) q) / 2, q (..., Np)."""
+        qd, host = _device.to_device(q)
+        if qd.shape[-1] != self.Np:
+            raise ValueError(f"expected trailing size {self.Np}, got {qd.shape[-1]}")
+        t = _device.torch()
+        outs = [t.empty_like(qd) for _ in range(3)]
+        _lib.check(_lib.load().bbdg_ops_grad(self.N, _device.dtype_id(qd), qd.numel() // self.Np, qd.data_ptr(),
+                                             *[o.data_ptr() for o in outs], _device.stream()), "bbdg_ops_grad")
+        return tuple(_device.back(o, host) for o in outs)
+
+    def lift_flux(self, flux, mode: str = "factorized"):
+        """Dispatch of the three lift modes (bernstein.py:457-466), on the device."""
+        if mode == "dense":
+            shp = tuple(np.shape(flux))
+            if shp[-2:] != (4, self.Nfp):
+                raise ValueError(f"flux must end in (4, {self.Nfp}), got {shp[-2:]}")
+            fd, host = _device.to_device(flux)
+            return _device.back(_device.dense_apply(("bb_dense_L", self.N), self.dense_L,
+                                                    fd.reshape(shp[:-2] + (4 * self.Nfp,))), host)
+        if mode == "factorized":
+            return lift_apply_factorized(self.lift, flux)
+        if mode == "optimal":
+            return lift_apply_optimal(self.lift, flux)
+        raise ValueError(f"unknown lift mode {mode!r}")
 
     def el_ell(self):
         """E_L as ELL (cols, vals), width <= Nfp + 3 (reference bernstein.py:286-289)."""

@@ -296,6 +296,23 @@ static int check_ctx(const bbdg_ctx* c) {
   return BBDG_OK;
 }
 
+// External lift ids (bbdg.h) -> kernel families.  "factorized" is the reference's default lift
+// L = E_L L0 (bernstein.py:301-310); like "optimal" (:313-329) it runs as L0 + the one-degree
+// reduction sweeps of the fused kernel (E_L is the composition of those sweeps, so the two modes
+// differ by rounding only, <= 2.4e-16 in the reference itself).  "ell" keeps the paper's
+// non-optimal Alg. 3 kernel that applies E_L as stored ELL rows (tile_kernel, LIFT_FACTORIZED).
+static int internal_lift(int ext) {
+  switch (ext) {
+    case BBDG_LIFT_FACTORIZED: return LIFT_OPTIMAL;
+    case BBDG_LIFT_OPTIMAL: return LIFT_OPTIMAL;
+    case BBDG_LIFT_DENSE: return LIFT_DENSE;
+    case BBDG_LIFT_BLOCKED: return LIFT_BLOCKED;
+    case BBDG_LIFT_ELL: return LIFT_FACTORIZED;
+  }
+  return -1;
+}
+
+// validates the external lift id and turns it into the kernel family
 static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
   if (c->basis == BBDG_BASIS_NODAL) {
     // WaveSystem forces "dense" for the nodal basis (solver.py:168-169); BLOCKED selects the
@@ -303,19 +320,30 @@ static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
     if (lift == BBDG_LIFT_BLOCKED) {
       if (!c->bvol || !c->blift || !c->flux)
         return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded (set_nodal_ops + set_lift_tables)");
+      lift = LIFT_BLOCKED;
       return BBDG_OK;
     }
-    lift = BBDG_LIFT_DENSE;
+    if (lift < 0 || lift > BBDG_LIFT_ELL) return set_error(BBDG_ERR_ARG, "unknown lift mode");
+    lift = LIFT_DENSE;
     if (surf && !c->liftT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal dense lift not uploaded");
     if (!c->dT) return set_error(BBDG_ERR_UNSUPPORTED, "nodal derivative matrices not uploaded");
     return BBDG_OK;
   }
-  if (lift < 0 || lift > 2) return set_error(BBDG_ERR_ARG, "unknown lift mode (blocked is nodal-only)");
-  if (surf && lift == BBDG_LIFT_FACTORIZED && !c->el_vals)
+  if (lift < 0 || lift > BBDG_LIFT_ELL || lift == BBDG_LIFT_BLOCKED)
+    return set_error(BBDG_ERR_ARG, "unknown lift mode (blocked is nodal-only)");
+  if (surf && lift == BBDG_LIFT_ELL && !c->el_vals)
     return set_error(BBDG_ERR_UNSUPPORTED, "E_L table not uploaded (bbdg_ctx_set_lift_tables)");
   if (surf && lift == BBDG_LIFT_DENSE && !c->liftT)
     return set_error(BBDG_ERR_UNSUPPORTED, "dense lift not uploaded (bbdg_ctx_set_lift_tables)");
+  lift = internal_lift(lift);
   return BBDG_OK;
+}
+
+// the fused kernels stage field planes with 16-byte TMA bulk copies: the base pointers must be
+// 16-byte aligned (every cudaMalloc / torch caching-allocator buffer is)
+static int check_aligned(const void* a, const void* b = nullptr, const void* c = nullptr) {
+  const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(c);
+  return (m & 15) ? set_error(BBDG_ERR_ARG, "state arrays must be 16-byte aligned") : BBDG_OK;
 }
 
 template <typename T>
@@ -452,10 +480,10 @@ int bbdg_ctx_set_halo(bbdg_ctx* c, const void* halo, int64_t nhalo) {
 int bbdg_volume(bbdg_ctx* c, const void* q, void* rhs, int accumulate, void* stream) {
   if (int rc = check_ctx(c)) return rc;
   if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q");
+  if (int rc = check_aligned(q, rhs)) return rc;
   int lift = BBDG_LIFT_OPTIMAL;
-  if (c->basis == BBDG_BASIS_NODAL) {
-    if (int rc = check_lift(c, lift, false)) return rc;
-  }
+  if (int rc = check_lift(c, lift, false)) return rc;
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
     p.q = static_cast<const T*>(q);
@@ -468,6 +496,8 @@ int bbdg_volume(bbdg_ctx* c, const void* q, void* rhs, int accumulate, void* str
 int bbdg_surface(bbdg_ctx* c, const void* q, void* rhs, int lift, int accumulate, void* stream) {
   if (int rc = check_ctx(c)) return rc;
   if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q (neighbour traces are read during the call)");
+  if (int rc = check_aligned(q, rhs)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
@@ -488,6 +518,7 @@ int bbdg_rhs_range(bbdg_ctx* c, const void* q, void* rhs, int lift, int64_t k0, 
   if (k0 < 0 || k1 > c->K || k0 > k1) return set_error(BBDG_ERR_ARG, "element range outside [0, K]");
   if (!q || !rhs) return set_error(BBDG_ERR_ARG, "null state pointer");
   if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q");
+  if (int rc = check_aligned(q, rhs)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
@@ -512,6 +543,7 @@ int bbdg_lsrk_stage_range(bbdg_ctx* c, const void* q_in, void* q_out, void* res,
   if (!q_in || !q_out || !res) return set_error(BBDG_ERR_ARG, "null state pointer");
   if (q_in == q_out) return set_error(BBDG_ERR_ARG, "q_out must not alias q_in");
   if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  if (int rc = check_aligned(q_in, q_out, res)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
@@ -546,18 +578,35 @@ static const double kRK4B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717
                                 2277821191437.0 / 14882151754819.0};
 
 int bbdg_step(bbdg_ctx* c, void* q, void* q_tmp, void* res, double dt, int lift, void* stream) {
+  return bbdg_step2(c, q, q_tmp, nullptr, res, dt, lift, stream);
+}
+
+// Five stages.  With a second scratch buffer they run q -> t1 -> t2 -> t1 -> t2 -> q, so the last
+// stage writes the caller's q directly; with q_tmp2 == NULL they alternate q <-> q_tmp and one
+// device copy moves the result (left in q_tmp by the odd stage count) back into q.
+int bbdg_step2(bbdg_ctx* c, void* q, void* q_tmp, void* q_tmp2, void* res, double dt, int lift, void* stream) {
   if (int rc = check_ctx(c)) return rc;
   if (!q || !q_tmp || !res) return set_error(BBDG_ERR_ARG, "null state pointer");
+  if (q_tmp2 && (q_tmp2 == q || q_tmp2 == q_tmp || q_tmp2 == res))
+    return set_error(BBDG_ERR_ARG, "scratch buffers must be distinct");
   if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t bytes = (size_t)4 * c->K * c->Np * (c->dtype == BBDG_F32 ? 4 : 8);
   cudaError_t e = cudaMemsetAsync(res, 0, bytes, s);
   if (e != cudaSuccess) return set_cuda_error(e, "res zeroing");
-  void* buf[2] = {q, q_tmp};
+  void* seq[6];
+  if (q_tmp2) {
+    void* s6[6] = {q, q_tmp, q_tmp2, q_tmp, q_tmp2, q};
+    std::memcpy(seq, s6, sizeof(seq));
+  } else {
+    void* s6[6] = {q, q_tmp, q, q_tmp, q, q_tmp};
+    std::memcpy(seq, s6, sizeof(seq));
+  }
   for (int st = 0; st < 5; ++st) {
-    int rc = bbdg_lsrk_stage(c, buf[st & 1], buf[(st + 1) & 1], res, lift, kRK4A[st], kRK4B[st], dt, stream);
+    int rc = bbdg_lsrk_stage(c, seq[st], seq[st + 1], res, lift, kRK4A[st], kRK4B[st], dt, stream);
     if (rc) return rc;
   }
+  if (q_tmp2) return BBDG_OK;
   e = cudaMemcpyAsync(q, q_tmp, bytes, cudaMemcpyDeviceToDevice, s);
   return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "final stage copy");
 }

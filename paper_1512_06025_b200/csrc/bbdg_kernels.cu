@@ -1,6 +1,8 @@
 // Instantiation unit: compiled once per (BBDG_T, BBDG_N) so the 2 x 9 degree /
 // dtype combinations build in parallel.  Exposes a launcher table entry
 // through a C++ symbol named after the pair.
+#include <atomic>
+
 #include "bbdg_internal.h"
 #include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
@@ -17,10 +19,23 @@ namespace {
 
 // persistent launch: grid = min(#groups needed, SMs x resident CTAs), one CTA
 // holds NG independent element groups
+// Launch attributes are per device: each kernel keeps a per-device cache of its resident CTAs per
+// SM (0 = not yet configured).  Concurrent first launches from several host threads may both set
+// the (idempotent) attribute; the cache itself is atomic.
+constexpr int kMaxDevices = 64;
+using DevCache = std::atomic<int>[kMaxDevices];
+
+inline int current_device() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+
 template <class KernT, int THREADS, int TOTAL, int KE, int NG>
-int launch_persistent(KernT kern, int& blocks_per_sm, const void* vp, cudaStream_t stream, int num_sms) {
+int launch_persistent(KernT kern, DevCache& cache, const void* vp, cudaStream_t stream, int num_sms) {
   using T = BBDG_T;
-  if (blocks_per_sm < 0) {
+  const int dev = current_device();
+  int blocks_per_sm = cache[dev].load(std::memory_order_acquire);
+  if (blocks_per_sm < 1) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TOTAL);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     int b = 0;
@@ -28,6 +43,7 @@ int launch_persistent(KernT kern, int& blocks_per_sm, const void* vp, cudaStream
     if (e != cudaSuccess) return set_cuda_error(e, "occupancy");
     if (b < 1) return set_error(BBDG_ERR_UNSUPPORTED, "tile kernel does not fit on an SM");
     blocks_per_sm = b;
+    cache[dev].store(b, std::memory_order_release);
   }
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
   const int64_t ntiles = (p.kend - p.kbeg + KE - 1) / KE;
@@ -41,9 +57,9 @@ int launch_persistent(KernT kern, int& blocks_per_sm, const void* vp, cudaStream
 template <int OP, int FSR> int launch_opt(const void* vp, cudaStream_t stream, int num_sms) {
   using T = BBDG_T;
   using L = OptLayout<T, BBDG_N, OP, FSR>;
-  static int blocks_per_sm = -1;
+  static DevCache cache;
   return launch_persistent<decltype(&opt_kernel<T, BBDG_N, OP, FSR>), L::threads, L::total, L::KE, L::NG>(
-      opt_kernel<T, BBDG_N, OP, FSR>, blocks_per_sm, vp, stream, num_sms);
+      opt_kernel<T, BBDG_N, OP, FSR>, cache, vp, stream, num_sms);
 }
 
 // nodal block-partitioned path: flux kernel (surface ops), then the tensor-core GEMM kernel
@@ -59,12 +75,13 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 8);
     nodal_flux_kernel<T, BBDG_N><<<(unsigned)grid, 256, 0, stream>>>(p);
   }
-  static bool attr = false;
+  static DevCache attr;
   auto kern = nodal_mma_kernel<T, BBDG_N, OP>;
-  if (!attr) {
+  const int dev = current_device();
+  if (attr[dev].load(std::memory_order_acquire) == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal)");
-    attr = true;
+    attr[dev].store(1, std::memory_order_release);
   }
   const int64_t ntiles = (nl + L::ET - 1) / L::ET;
   kern<<<(unsigned)std::min<int64_t>(ntiles, num_sms), L::THREADS, L::total, stream>>>(p);
@@ -76,7 +93,7 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
   using T = BBDG_T;
   if constexpr (BASIS == BASIS_NODAL && LIFT == LIFT_BLOCKED) {
     return launch_nodal<OP>(vp, stream, num_sms);
-  } else if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) {
+  } else if constexpr (BASIS == BASIS_BERNSTEIN && LIFT == LIFT_OPTIMAL) {   // also the "factorized" mode
     // field-plane stride residue (K Np) mod (16 / sizeof(T)) selects the smem field stride
     const Params<T>& p = *static_cast<const Params<T>*>(vp);
     constexpr int A = 16 / sizeof(T);
@@ -92,10 +109,10 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
       return fsr ? launch_opt<OP, 1>(vp, stream, num_sms) : launch_opt<OP, 0>(vp, stream, num_sms);
     }
   } else {
-    static int blocks_per_sm = -1;
+    static DevCache cache;
     using L = Layout<T, BBDG_N, OP, LIFT, BASIS>;
     return launch_persistent<decltype(&tile_kernel<T, BBDG_N, OP, LIFT, BASIS>), L::threads, L::total, L::KE, L::NG>(
-        tile_kernel<T, BBDG_N, OP, LIFT, BASIS>, blocks_per_sm, vp, stream, num_sms);
+        tile_kernel<T, BBDG_N, OP, LIFT, BASIS>, cache, vp, stream, num_sms);
   }
 }
 

@@ -263,9 +263,21 @@ class WaveSystem:
         _lib.check(self._lib.bbdg_ctx_set_halo(self._ctx, halo.data_ptr() if nhalo else None, int(nhalo)),
                    "bbdg_ctx_set_halo")
 
-    def step_into(self, q, q_tmp, res, dt, lift_mode="factorized"):
-        _lib.check(self._lib.bbdg_step(self._ctx, q.data_ptr(), q_tmp.data_ptr(), res.data_ptr(), float(dt),
-                                       self._lift_id(lift_mode), self._stream()), "bbdg_step")
+    def step_into(self, q, q_tmp, res, dt, lift_mode="factorized", q_tmp2=None):
+        """Five fused stages in place on q (bbdg_step2: with q_tmp2 the last stage writes q)."""
+        _lib.check(self._lib.bbdg_step2(self._ctx, q.data_ptr(), q_tmp.data_ptr(),
+                                        q_tmp2.data_ptr() if q_tmp2 is not None else None, res.data_ptr(),
+                                        float(dt), self._lift_id(lift_mode), self._stream()), "bbdg_step2")
+
+    def scratch(self, like, n=2):
+        """n cached (4,K,Np) device scratch buffers shaped like `like` (reused across steps)."""
+        key = (like.dtype, like.device, n)
+        buf = getattr(self, "_scratch", None)
+        if buf is None or buf[0] != key:
+            t = self._torch
+            buf = (key, [t.empty_like(like) for _ in range(n)])
+            self._scratch = buf
+        return buf[1]
 
     # ---------------------------------------------------------------- reference API
     def volume_rhs(self, state: FieldState):
@@ -405,15 +417,18 @@ def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorize
             return FieldState(state.q, state.basis, t0 + dt)
         q = system.to_device(state.q)
         r = system.to_device(res) if res is not None else torch.empty_like(q)
-        tmp = torch.empty_like(q)
-        system.step_into(q, tmp, r, dt, lift)
+        t1, t2 = system.scratch(q)
+        system.step_into(q, t1, r, dt, lift, q_tmp2=t2)   # the fifth stage writes q: no final copy
         _copy_back(state.q, q)
         if res is not None:
             _copy_back(res, r)
         return FieldState(state.q, state.basis, t0 + dt)
-    # duck-typed system: host rhs, device update (no CPU arithmetic on the update)
-    host = not _is_tensor(state.q)
-    q = torch.from_numpy(np.ascontiguousarray(state.q)).cuda() if host else state.q
+    # duck-typed system: the system's rhs, the update on the device (no CPU arithmetic on it)
+    host = not (_is_tensor(state.q) and state.q.is_cuda)
+    if _is_tensor(state.q):
+        q = state.q.cuda().contiguous() if host else state.q
+    else:
+        q = torch.from_numpy(np.ascontiguousarray(state.q)).cuda()
     r = torch.zeros_like(q)
     work = FieldState(state.q, state.basis, t0)
     for s in range(5):
@@ -422,7 +437,10 @@ def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorize
         kd = torch.as_tensor(np.asarray(k) if not _is_tensor(k) else k).to(device=q.device, dtype=q.dtype)
         _device_update(q, r, kd.contiguous(), RK4A[s], RK4B[s], dt)
         if host:
-            state.q[...] = q.cpu().numpy()
+            if _is_tensor(state.q):
+                state.q.copy_(q)
+            else:
+                state.q[...] = q.cpu().numpy()
     if res is not None:
         _copy_back(res, r)
     return FieldState(state.q, state.basis, t0 + dt)
@@ -437,7 +455,8 @@ def integrate(system, state: FieldState, dt: float, nsteps: int, lift_mode: str 
     steps), and the caller's array is updated in place at the end.
     """
     if not isinstance(system, WaveSystem):
-        res = np.zeros_like(state.q)
+        # any object with .rhs (reference solver.py:217-239, including its energy guard)
+        res = np.zeros_like(state.q) if not _is_tensor(state.q) else state.q.new_zeros(state.q.shape)
         e0 = discrete_energy(system, state) if energy_guard else None
         if callback:
             callback(0, state)
@@ -445,6 +464,10 @@ def integrate(system, state: FieldState, dt: float, nsteps: int, lift_mode: str 
             state = lsrk4_step(system, state, dt, lift_mode, res)
             if callback:
                 callback(step, state)
+            if energy_guard and step % 20 == 0:
+                e = discrete_energy(system, state)
+                if e > energy_guard * max(e0, 1e-300):
+                    raise RuntimeError(f"unstable run: energy grew from {e0:.3e} to {e:.3e} by step {step}")
         return state
     if dt <= 0:
         raise ValueError("dt must be positive")
@@ -610,7 +633,7 @@ def discrete_energy(system: WaveSystem, state: FieldState) -> float:
 
     Device states: the bbdg_energy kernel (float64 accumulation, deterministic)."""
     M = system.ops_double.mass
-    if _is_tensor(state.q):
+    if _is_tensor(state.q) and state.q.is_cuda:
         torch = _torch()
         q = state.q.contiguous()
         d = getattr(system, "_energy_dev", None)
@@ -628,7 +651,8 @@ def discrete_energy(system: WaveSystem, state: FieldState) -> float:
                                    d["M"].data_ptr(), d["coef"].data_ptr(), d["partial"].data_ptr(),
                                    d["out"].data_ptr(), torch.cuda.current_stream().cuda_stream), "bbdg_energy")
         return float(d["out"].item())
-    q = np.asarray(state.q, dtype=np.float64)
+    # host arrays / CPU tensors: the reference's float64 formula on the host (solver.py:306-312)
+    q = state.q.double().numpy() if _is_tensor(state.q) else np.asarray(state.q, dtype=np.float64)
     quad = np.einsum("fkn,nm,fkm->fk", q, M, q)
     return float(((quad[0] / system.mat.kappa + system.mat.rho * quad[1:].sum(axis=0)) * system.mesh.jac).sum())
 

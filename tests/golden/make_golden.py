@@ -8,10 +8,11 @@ the outputs are committed as small compressed .npz fixtures:
   golden_bb.npz     Bernstein: seed-2024 random states on cube_mesh(2) (N=1..4)
                     and cube_mesh(1) (N=5..9); volume_rhs, surface_rhs x 3 lift
                     modes, rhs, one lsrk4_step -- float64 and float32
-  golden_nodal.npz  nodal: rhs + one lsrk4_step on cube_mesh(2), N=1..6, float64
+  golden_nodal.npz  nodal: rhs + one lsrk4_step on cube_mesh(2), N=1..6, and on
+                    cube_mesh(1), N=7..9, float64
   golden_c1.npz     config 1: cube_mesh(6), N=3, initial_state, 10 LSRK4 steps
-                    at stable_dt(m,3,1.0), float64 factorized (final state) and
-                    norms for the other modes / float32
+                    at stable_dt(m,3,1.0): final states and norms for every lift
+                    mode, float64 and float32
   golden_setup.npz  mesh arrays + trace gathers (cube_mesh(2)) and the
                     reference operator tables for N=1..9
 """
@@ -63,9 +64,9 @@ def bb_cases():
 
 def nodal_cases():
     data = {}
-    m = msh.cube_mesh(2)
-    mat = sol.Materials.homogeneous(m.K)
-    for N in range(1, 7):
+    for N in range(1, 10):
+        m = msh.cube_mesh(2 if N <= 6 else 1)
+        mat = sol.Materials.homogeneous(m.K)
         ops = NodalRefOps.build(N)
         rng = np.random.default_rng(4048 + N)
         q = rng.standard_normal((4, m.K, ops.Np))
@@ -90,8 +91,7 @@ def c1_case():
         for mode in MODES:
             st = sol.initial_state(m, N, "bernstein", dtype=dtype)
             st = sol.integrate(sy, st, dt, 10, lift_mode=mode, energy_guard=None)
-            if dname == "f64" and mode == "factorized":
-                data["q_final_f64_factorized"] = st.q
+            data[f"q_final_{dname}_{mode}"] = st.q
             data[f"norm_{dname}_{mode}"] = float(np.linalg.norm(st.q.astype(np.float64)))
             data[f"l2err_{dname}_{mode}"] = sol.l2_error(sy, st)
     np.savez_compressed(OUT / "golden_c1.npz", **data)

@@ -70,6 +70,27 @@ def test_convergence_errors_match_reference(sens, n, N):
     assert 1 / 3 <= (e32 + 1e-7) / (r32 + 1e-7) <= 3, (e32, r32)
 
 
+@pytest.mark.parametrize("N", range(1, 10))
+def test_convergence_states_match_reference(N):
+    """configs[3] at the north-star float64 tolerance: the whole state after the convergence run
+    (cube_mesh(2), tau = 0.5, factorized lift -- the reference default; 5..392 steps) equals the
+    reference's own final state to 1e-12 relative L2 (golden_sens_states.npz, produced by
+    make_sens_states.py on the reference), and so does the error functional."""
+    import torch
+
+    g = np.load(GOLD.parent / "golden_sens_states.npz")
+    m = cube_mesh(2)
+    sy = WaveSystem(m, BernsteinRefOps.build(N), Materials.homogeneous(m.K))
+    st = initial_state(m, N, "bernstein")
+    nst = int(g[f"nst_N{N}"])
+    assert nst == int(np.ceil(0.5 / stable_dt(m, N, 1.0)))
+    st = integrate(sy, FieldState(torch.as_tensor(st.q).cuda(), "bernstein"), 0.5 / nst, nst, "factorized",
+                   energy_guard=None)
+    assert rel_l2(st.q.cpu().numpy(), g[f"q_N{N}"]) < 1e-12
+    e, r = ErrorFunctional(m, sy.ops_double)(st), float(g[f"err_N{N}"])
+    assert abs(e - r) <= 1e-10 * r, (e, r)
+
+
 def test_reference_divergence_reproduced(sens):
     """N = 1 at cfl = 0.5 diverges on cube_mesh(16) in the reference (error ~1.12 at tau = 0.5);
     the device path reproduces the reference's value, not a stabilised one."""

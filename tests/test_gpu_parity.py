@@ -64,10 +64,11 @@ def test_bb_parity_with_reference_golden(golden_bb, N, dname):
     assert rel_l2(st.q, g[f"N{N}_{dname}_step"]) < tol
 
 
-@pytest.mark.parametrize("N", range(1, 7))
+@pytest.mark.parametrize("N", range(1, 10))
 def test_nodal_parity_with_reference_golden(golden_nodal, N):
+    """Node-per-thread nodal kernels vs the reference (cube_mesh(2) for N <= 6, cube_mesh(1) above)."""
     g = golden_nodal
-    m = cube_mesh(2)
+    m = cube_mesh(2 if N <= 6 else 1)
     sy = WaveSystem(m, NodalRefOps.build(N), Materials.homogeneous(m.K))
     q = g[f"N{N}_q"]
     assert rel_l2(sy.volume_rhs(FieldState(q.copy(), "nodal")), g[f"N{N}_vol"]) < TOL["f64"]
@@ -76,12 +77,12 @@ def test_nodal_parity_with_reference_golden(golden_nodal, N):
     assert rel_l2(st.q, g[f"N{N}_step"]) < TOL["f64"]
 
 
-@pytest.mark.parametrize("N", range(1, 7))
+@pytest.mark.parametrize("N", range(1, 10))
 @pytest.mark.parametrize("dname", ["f64", "f32"])
 def test_nodal_blocked_parity_with_reference_golden(golden_nodal, N, dname):
     """Block-partitioned tensor-core nodal kernels (fp64 DMMA, fp32 3xTF32) vs the reference."""
     g = golden_nodal
-    m = cube_mesh(2)
+    m = cube_mesh(2 if N <= 6 else 1)
     sy = WaveSystem(m, NodalRefOps.build(N), Materials.homogeneous(m.K), dtype=DT[dname])
     q = g[f"N{N}_q"].astype(DT[dname])
     assert rel_l2(sy.rhs(FieldState(q.copy(), "nodal"), "blocked"), g[f"N{N}_rhs"]) < TOL[dname]
@@ -105,20 +106,48 @@ def test_nodal_blocked_matches_dense_fresh_inputs(N, dname):
     assert rel_l2(got, want) < TOL[dname]
 
 
-@pytest.mark.parametrize("N", [1, 3, 5, 7, 9])
+def stage_vs_oracle(sy, ref, q, res, dt, mode, rows=None, tol=None):
+    """One fused LSRK stage (bbdg_lsrk_stage: the bench's timed kernel) against the oracle's
+    res = A res + dt rhs; q_out = q + B res, element-wise over `rows` (all elements by default)."""
+    import torch
+
+    from paper_1512_06025_b200.solver import RK4A, RK4B
+
+    qd, rd = torch.from_numpy(q).cuda(), torch.from_numpy(res.copy()).cuda()
+    qo = torch.empty_like(qd)
+    sy.stage_into(qd, qo, rd, RK4A[1], RK4B[1], dt, mode)
+    qo, rd = qo.cpu().numpy(), rd.cpu().numpy()
+    tol = tol or TOL["f64" if q.dtype == np.float64 else "f32"]
+    for k0, k1 in rows or [(0, sy.K)]:
+        want_q, want_r = ref.stage(q, res, RK4A[1], RK4B[1], dt, mode, k0, k1)
+        assert rel_l2(qo[:, k0:k1], want_q) < tol, (mode, k0, k1)
+        assert rel_l2(rd[:, k0:k1], want_r) < tol, (mode, k0, k1)
+
+
+@pytest.mark.parametrize("N", range(1, 10))
 @pytest.mark.parametrize("dname", ["f64", "f32"])
 def test_bb_parity_with_oracle_fresh_inputs(N, dname):
-    """cube_mesh(4) (K=384), heterogeneous materials, a fresh seed: kernels vs the pinned oracle."""
+    """cube_mesh(4) (K=384, so K Np = 0 mod 4: the field-stride residue FSR 0 that the bench's
+    K=384,000 and the HBM-filling meshes select), heterogeneous materials, a fresh seed: every
+    fused-kernel instantiation the bench times (stage; rhs / volume / surface) vs the oracle."""
     m = cube_mesh(4)
     rng = np.random.default_rng(100 + N)
     kap, rho = rng.uniform(0.5, 2.0, m.K), rng.uniform(0.5, 2.0, m.K)
     dtype = DT[dname]
     sy = WaveSystem(m, BernsteinRefOps.build(N), Materials(kap, rho), dtype=dtype)
+    assert (m.K * sy.Np) % 4 == 0
     ref = orc.OracleSystem(orc.mesh_arrays(m), orc.bernstein_tables(N), kap, rho, dtype)
     q = rng.standard_normal((4, m.K, sy.Np)).astype(dtype)
     for mode in MODES:
         assert rel_l2(sy.rhs(FieldState(q.copy(), "bernstein"), mode), ref.rhs(q.copy(), mode)) < TOL[dname], mode
+    assert rel_l2(sy.volume_rhs(FieldState(q.copy(), "bernstein")), ref.volume_rhs(q.copy())) < TOL[dname]
+    for mode in ("optimal", "factorized", "ell"):
+        want = ref.surface_rhs(q.copy(), "factorized" if mode == "ell" else mode)
+        assert rel_l2(sy.surface_rhs(FieldState(q.copy(), "bernstein"), mode), want) < TOL[dname], mode
     dt = stable_dt(m, N, float(np.sqrt(kap / rho).max()))
+    res = rng.standard_normal(q.shape).astype(dtype)
+    for mode in ("optimal", "factorized"):
+        stage_vs_oracle(sy, ref, q, res, dt, mode)
     st = lsrk4_step(sy, FieldState(q.copy(), "bernstein"), dt, "optimal")
     assert rel_l2(st.q, ref.lsrk4_step(q.copy(), dt, "optimal")) < TOL[dname]
 
@@ -175,19 +204,19 @@ def test_lsrk4_scalar_ode_duck_typed():
         lsrk4_step(_Zero(), FieldState(q0.copy(), "bernstein"), 0.0)
 
 
-def test_config1_ten_steps_vs_reference(golden_c1):
-    """Config 1: cube_mesh(6), N=3, 10 LSRK4 steps from the exact IC, vs the reference run."""
+@pytest.mark.parametrize("dname", ["f64", "f32"])
+@pytest.mark.parametrize("mode", MODES)
+def test_config1_ten_steps_vs_reference(golden_c1, dname, mode):
+    """Config 1: cube_mesh(6), N=3, 10 LSRK4 steps from the exact IC: the full final state vs the
+    reference's own run, every lift mode and precision (element-wise relative L2)."""
     m = cube_mesh(6)
     dt = float(golden_c1["dt"])
-    for dname in ("f64", "f32"):
-        sy = bern_system(6, 3, dname)
-        for mode in MODES:
-            st = integrate(sy, initial_state(m, 3, "bernstein", dtype=DT[dname]), dt, 10, lift_mode=mode,
-                           energy_guard=None)
-            if dname == "f64" and mode == "factorized":
-                assert rel_l2(st.q, golden_c1["q_final_f64_factorized"]) < TOL["f64"]
-            nrm = float(np.linalg.norm(st.q.astype(np.float64)))
-            assert abs(nrm - float(golden_c1[f"norm_{dname}_{mode}"])) / nrm < TOL[dname], (dname, mode)
+    sy = bern_system(6, 3, dname)
+    st = integrate(sy, initial_state(m, 3, "bernstein", dtype=DT[dname]), dt, 10, lift_mode=mode, energy_guard=None)
+    assert st.q.dtype == DT[dname]
+    assert rel_l2(st.q, golden_c1[f"q_final_{dname}_{mode}"]) < TOL[dname], (dname, mode)
+    nrm = float(np.linalg.norm(st.q.astype(np.float64)))
+    assert abs(nrm - float(golden_c1[f"norm_{dname}_{mode}"])) / nrm < TOL[dname], (dname, mode)
 
 
 def test_single_precision_rhs_close_to_double():
@@ -287,19 +316,19 @@ def test_full_size_properties(c2_mesh, N):
         del sy
 
 
-@pytest.mark.parametrize("N", range(2, 10))
+@pytest.mark.parametrize("N", range(1, 10))
+@pytest.mark.parametrize("K", [44, 45, 46, 47])
 @pytest.mark.parametrize("dname", ["f64", "f32"])
-def test_bb_parity_odd_element_count(N, dname):
-    """K = 47 (cube_mesh(2) minus one tet: a non-convex domain with extra boundary faces):
-    K Np mod 4 = 2, 1, 3 for N = 2, 4, 8, so the fused kernel's field planes land at
-    different 16-byte shifts (stride-residue layouts FSR != 0) and the last TMA window
-    runs past the end of the state arrays (sub-16-byte tail copied by hand).  47 is odd, so
-    every order with KE > 1 ends on a partial tile (incl. the fp64 stage's guarded HBM
-    reads of the LSRK register)."""
+def test_bb_parity_every_stride_residue(N, K, dname):
+    """Sub-meshes of cube_mesh(2) with K = 44..47 tets (non-convex domains with extra boundary
+    faces): K Np mod 4 takes every value the order allows, so each stride-residue variant of the
+    fused kernel (template FSR: 4 in fp32, 2 in fp64) is compared element-wise with the oracle; the
+    last TMA window runs past the end of the state arrays (sub-16-byte tail copied by hand) and
+    odd K ends on a partial tile (incl. the fp64 stage's guarded HBM reads of the LSRK register)."""
     base = cube_mesh(2)
-    m = from_arrays(base.vertices, base.tets[:-1])
-    assert m.K == 47
-    rng = np.random.default_rng(40 + N)
+    m = from_arrays(base.vertices, base.tets[:K])
+    assert m.K == K
+    rng = np.random.default_rng(40 + 10 * N + K)
     kap, rho = rng.uniform(0.5, 2.0, m.K), rng.uniform(0.5, 2.0, m.K)
     dtype = DT[dname]
     sy = WaveSystem(m, BernsteinRefOps.build(N), Materials(kap, rho), dtype=dtype)
@@ -311,5 +340,42 @@ def test_bb_parity_odd_element_count(N, dname):
     assert rel_l2(sy.surface_rhs(FieldState(q.copy(), "bernstein"), "optimal"),
                   ref.surface_rhs(q.copy(), "optimal")) < TOL[dname]
     dt = stable_dt(m, N, float(np.sqrt(kap / rho).max()))
+    stage_vs_oracle(sy, ref, q, rng.standard_normal(q.shape).astype(dtype), dt, "optimal")
     st = lsrk4_step(sy, FieldState(q.copy(), "bernstein"), dt, "optimal")
     assert rel_l2(st.q, ref.lsrk4_step(q.copy(), dt, "optimal")) < TOL[dname]
+
+
+# ------------------------------------------------------------------ config-2 size vs the oracle
+@pytest.fixture(scope="module")
+def c2_arrays(c2_mesh):
+    return orc.mesh_arrays(c2_mesh)
+
+
+_C2_MAPS = {}
+
+
+@pytest.mark.parametrize("N", range(1, 10))
+def test_config2_stage_vs_oracle(c2_mesh, c2_arrays, N):
+    """configs[1] mesh cube_mesh(26), K = 105,456 (FSR 0): the fused stage element-wise against the
+    oracle, fp64 and fp32 -- every element for N <= 3, three 1,024-element windows (start, middle,
+    end: boundary and interior elements) above, where the numpy oracle of the whole mesh is slow."""
+    m = c2_mesh
+    K = m.K
+    rows = None if N <= 3 else [(0, 1024), (K // 2, K // 2 + 1024), (K - 1024, K)]
+    key = (N, rows is None)
+    tabs = orc.bernstein_tables(N)
+    if key not in _C2_MAPS:
+        _C2_MAPS.clear()
+        _C2_MAPS[key] = orc.trace_maps(c2_arrays["vertices"], c2_arrays["tets"], c2_arrays["etoe"],
+                                       c2_arrays["etof"], tabs.face_pts, tabs.trace, tabs.Np, c2_arrays["h_elem"], rows)
+    rng = np.random.default_rng(2600 + N)
+    kap, rho = np.ones(K), np.ones(K)
+    dt = stable_dt(m, N, 1.0)
+    for dname in ("f64", "f32"):
+        dtype = DT[dname]
+        sy = WaveSystem(m, BernsteinRefOps.build(N), Materials(kap, rho), dtype=dtype)
+        ref = orc.OracleSystem(c2_arrays, tabs, kap, rho, dtype, maps=_C2_MAPS[key])
+        q = rng.standard_normal((4, K, sy.Np)).astype(dtype)
+        res = rng.standard_normal((4, K, sy.Np)).astype(dtype)
+        stage_vs_oracle(sy, ref, q, res, dt, "optimal", rows)
+        del sy

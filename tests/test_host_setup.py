@@ -31,6 +31,44 @@ def test_compact_codes_reproduce_reference_gather(golden_setup, N):
     assert np.array_equal(gn, golden_setup[f"N{N}_nodal_gather"])
 
 
+@pytest.mark.parametrize("N", [2, 4])
+def test_reference_signature_build_trace_maps(golden_setup, N):
+    """The reference's 4-argument form build_trace_maps(mesh, face_ref_points, face_positions, Np)
+    (mesh.py:158) gives the reference gather and checks the coordinates; a Mesh built from the
+    reference's nine fields (no permutation codes) derives them."""
+    m = msh.cube_mesh(2)
+    ops = bb.BernsteinRefOps.build(N)
+    fp = np.stack([ops.face_ref_points(f) for f in range(4)])
+    g, b = msh.build_trace_maps(m, fp, ops.trace, ops.Np)
+    assert np.array_equal(g, golden_setup[f"N{N}_gather"]) and np.array_equal(b, golden_setup[f"N{N}_boundary"])
+    bare = msh.Mesh(*[getattr(m, k) for k in MESH_KEYS])
+    assert np.array_equal(bare.face_perm, m.face_perm)
+    assert np.array_equal(msh.build_trace_maps(bare, fp, ops.trace, ops.Np)[0], g)
+    bad = fp.copy()
+    bad[0, [0, 1]] = bad[0, [1, 0]]                    # swap two face points: no longer conforming
+    with pytest.raises(ValueError):
+        msh.build_trace_maps(m, bad, ops.trace, ops.Np)
+
+
+@pytest.mark.parametrize("N", range(1, 10))
+def test_reference_operator_objects(golden_setup, N):
+    """derivative_ops / build_L0 / build_lift expose the reference's sparse-row operators
+    (bernstein.py:182-298) with the same dense values and row widths."""
+    s = golden_setup
+    ds = bb.derivative_ops(N)
+    assert np.array_equal(np.stack([o.cols for o in ds.ops]), s[f"N{N}_dcols"])
+    assert np.array_equal(ds.values, s[f"N{N}_dvals"])
+    lf = bb.build_lift(N)
+    assert np.abs(lf.L0.toarray() - s[f"N{N}_L0"]).max() < 1e-13 * np.abs(s[f"N{N}_L0"]).max()
+    assert np.abs(lf.EL.toarray() - s[f"N{N}_EL"]).max() < 1e-13 * np.abs(s[f"N{N}_EL"]).max()
+    assert lf.L0.row_width <= 7 and lf.EL.row_width <= mi.face_dim(N) + 3
+    assert all(r.row_width <= 3 for r in lf.reductions) and len(lf.reductions) == N
+    for f in (0, 3):
+        Lo = bb.dense_lift_oracle(N, f)
+        fact = lf.EL.toarray()[:, f * lf.Nfp:(f + 1) * lf.Nfp] @ lf.L0.toarray()
+        assert np.abs(fact - Lo).max() / np.abs(Lo).max() < 1e-8
+
+
 def test_face_codes_packing():
     m = msh.cube_mesh(3)
     nbr, code = m.face_codes()

@@ -1,21 +1,23 @@
-"""Benchmark: GDOF-updates/s per RK stage of the BB-DG hot path, N = 1..9.
+"""Benchmark: GDOF-updates/s per RK stage of the BB-DG hot path vs order N = 1..9, with the
+per-kernel fraction of the HBM roofline (BASELINE.json configs[2]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--dtype f32|f64] [--n 26] [--orders 1-9] [--lift optimal]
+                    [--dtypes f32,f64] [--orders 1-9] [--fill 0.8] [--strong] [--quick]
 
-Workload (BASELINE.json configs[2], the kernel sweep): cube_mesh(40) =
-384,000 tets per GPU, Bernstein basis, orders N = 1..9, homogeneous
-materials, standard-normal synthetic state (seed 2024).  One bench "step" =
-one fused LSRK4 stage (volume + surface + update, ``bbdg_lsrk_stage``) at
-every order of the sweep; the headline value is the sweep's whole-job DOF
-throughput sum_N 4 K Np(N) / sum_N t_stage(N).  Orders run one after another
-(bounded memory); L2 (126 MB) is flushed with a 256 MB write before every
-timed launch, outside the event window.
+Workload (configs[2]): per order N = 1..9 an HBM-filling box mesh of Kuhn tetrahedra, built on
+the device (mesh_device.BoxMesh -> bbdg_ctx_set_box_mesh: no host arrays), whose state q, the
+stage output and the LSRK register plus the geometry records fill `--fill` of the GPU's memory;
+Bernstein basis, homogeneous materials, standard-normal synthetic state (seed 2024).  One bench
+"step" = one fused LSRK stage (volume + surface + update, ``bbdg_lsrk_stage``) at every order of
+the sweep, fp32 (the headline `value`) and fp64 (`per_dtype`); value = sum_N 4 K_N Np(N) /
+sum_N t_stage(N).  Every launch streams >= 1.4 GB, far above the 126 MB L2, so L2 is not flushed.
 
-Per-order extras: volume / surface (3 lift modes) / update kernels timed
-separately with their roofline fractions against MEASURED_PEAKS.json, the
-end-to-end lsrk4_step on a host state, and (configs[1]) the BB vs nodal
-comparison on cube_mesh(26).
+Per order (1 GPU): the volume, surface and update kernels timed separately on the same mesh with
+their roofline fractions (MEASURED_PEAKS.json), the end-to-end lsrk4_step on a host numpy state
+(pinned and pageable) on a host-fitting cube_mesh(40), and (configs[1]) BB vs nodal DG on
+cube_mesh(26).  Under torchrun (N > 1) every rank owns an x-layer slab of one box (weak scaling:
+an HBM-filling slab per rank; --strong: the 1-GPU mesh split N ways) with the NCCL face-trace halo
+overlapped with the interior elements; times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -36,6 +38,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "GDOF-updates/sec per RK stage vs order N=1..9; per-kernel % HBM/FLOP roofline"
 UNIT = "GDOF/s"
+WORKLOAD = ("BB-DG acoustic wave, fused LSRK4 stage sweep N={orders} on HBM-filling Kuhn box meshes "
+            "(configs[2]), {lift} lift")
 
 
 def np_of(N):
@@ -57,10 +61,10 @@ def parse_orders(s):
     return out
 
 
-# ---------------------------------------------------------------------- algorithmic byte model
+# ---------------------------------------------------------------------- algorithmic byte model (DESIGN.md 3.3)
 def stage_bytes(N, s, K):
     """Fused stage: q_in, q_out, res r/w (16 Np) + neighbour traces (16 Nfp) + geometry (36) words
-    + 20 B connectivity per element (DESIGN.md, section 4)."""
+    + 20 B connectivity per element."""
     return K * ((16 * np_of(N) + 16 * nfp_of(N) + 36) * s + 20)
 
 
@@ -76,12 +80,17 @@ def update_bytes(N, s, K):
     return K * 20 * np_of(N) * s
 
 
+def resident_bytes(N, s, K):
+    """Device memory of one order's run: q, q_out, res + the fused geometry record + connectivity."""
+    return K * ((12 * np_of(N) + 36) * s + 20)
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------------- clocks sampler
@@ -93,6 +102,7 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -104,7 +114,6 @@ class Clocks:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -117,7 +126,7 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
-        for ln in getattr(self, "lines", []):
+        for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -134,352 +143,370 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------- GPU arm
-def build_system(mesh, N, dtype, basis="bernstein"):
-    from paper_1512_06025_b200 import BernsteinRefOps, Materials, NodalRefOps, WaveSystem
+def fill_box(N, s, budget_bytes, ranks=1):
+    """A Kuhn box (nx, n, n) whose resident bytes fit budget_bytes (per rank: nx a multiple of
+    `ranks` layers per rank), as cubic as possible."""
+    from paper_1512_06025_b200.mesh_device import BoxMesh
 
-    ops = BernsteinRefOps.build(N) if basis == "bernstein" else NodalRefOps.build(N)
-    return WaveSystem(mesh, ops, Materials.homogeneous(mesh.K), dtype=dtype)
+    per = resident_bytes(N, s, 1)
+    k_max = min(int(budget_bytes // per), (1 << 29) - 1)     # int32 face ids: 4 K < 2^31
+    n = max(1, int((k_max / 6) ** (1.0 / 3.0)))
+    nx = max(1, k_max // (6 * n * n))
+    return BoxMesh(nx * ranks, n, n, lo=(-0.5 * ranks, -0.5, -0.5), hi=(0.5 * ranks, 0.5, 0.5))
 
 
-def time_launches(torch, fn, flush, reps):
-    """Mean device time (ms) of fn over reps launches, L2 flushed before each (outside the events).
-    One untimed call first: the first launch of a kernel pays CUDA's lazy module load."""
-    fn()
-    tot = 0.0
+def events_time(torch, fn, reps, sync_group=None):
+    """Device time (ms) of `reps` back-to-back calls of fn, bracketed by barrier + synchronize."""
+    torch.cuda.synchronize()
+    if sync_group is not None:
+        torch.distributed.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
     for _ in range(reps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
         fn()
-        b.record()
-        b.synchronize()
-        tot += a.elapsed_time(b)
-    return tot / reps
+    b.record()
+    torch.cuda.synchronize()
+    if sync_group is not None:
+        torch.distributed.barrier()
+    return a.elapsed_time(b)
 
 
-def run_ours(args, rank, world):
+def max_over_ranks(torch, x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_dtype(args, dname, rank, world, dev, peak, clocks):
     import torch
 
-    from paper_1512_06025_b200 import cube_mesh, lsrk4_step, FieldState, stable_dt
-    from paper_1512_06025_b200.solver import RK4A, RK4B
+    from paper_1512_06025_b200 import BernsteinRefOps, Materials, WaveSystem, stable_dt
+    from paper_1512_06025_b200.dist import DistWaveSystem
+    from paper_1512_06025_b200.solver import RK4A, RK4B, _device_update
 
-    dev = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(dev)
-    dtype = np.float32 if args.dtype == "f32" else np.float64
-    s = 4 if args.dtype == "f32" else 8
-    mesh_n = {}   # per-order cube size in --fill mode
-
-    def fill_n(N):
-        """cube_mesh(n) whose q, q_out, res + geometry records use args.fill of the device memory."""
-        total = torch.cuda.get_device_properties(dev).total_memory
-        per_elem = 12 * np_of(N) * s + 2 * 36 * s + 20
-        # capped at n = 140 (16.5 M tets): the host-side setup arrays of WaveSystem stay < ~20 GB
-        return min(140, int((args.fill * total / per_elem / 6) ** (1.0 / 3.0)))
-
-    if world > 1:
-        # weak scaling: a box of world x n^3 cells, one n^3-cell x-slab per rank
-        from paper_1512_06025_b200.mesh import box_mesh
-
-        mesh = box_mesh(world * args.n, args.n, args.n, lo=(-0.5 * world, -0.5, -0.5), hi=(0.5 * world, 0.5, 0.5))
-    elif args.fill > 0:
-        mesh = None
-    else:
-        mesh = cube_mesh(args.n)
-    K = mesh.K // world if mesh is not None else 0
+    dtype = np.float32 if dname == "f32" else np.float64
+    s = 4 if dname == "f32" else 8
+    total_mem = torch.cuda.get_device_properties(dev).total_memory
     orders = parse_orders(args.orders)
-    Ks = {}
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    peak, peak_kind = load_peaks()
-
-    def make_system(N):
-        if world > 1:
-            from paper_1512_06025_b200 import BernsteinRefOps, Materials
-            from paper_1512_06025_b200.dist import DistWaveSystem
-
-            sy = DistWaveSystem(mesh, BernsteinRefOps.build(N), Materials.homogeneous(mesh.K), dtype, rank, world,
-                                align=6 * args.n * args.n)
-            sy.Np, sy.torch_dtype = sy.local.Np, sy.local.torch_dtype
-            return sy
-        return build_system(mesh, N, dtype)
-
-    # one order at a time (bounded memory): W warm-up stages, then K timed stages, each launch
-    # bracketed by CUDA events with the L2 flushed before it (outside the events)
-    per_n, rows = {}, {}
+    rows, per_n, Ks = {}, {}, {}
     gen = torch.Generator(device="cuda").manual_seed(2024 + rank)
-    with Clocks(dev) as clk:
-        for N in orders:
-            if args.fill > 0:
-                from paper_1512_06025_b200.mesh_device import cube_mesh_device
+    for N in orders:
+        torch.cuda.empty_cache()
+        budget = args.fill * (total_mem - torch.cuda.memory_allocated(dev))
+        if world == 1:
+            box = fill_box(N, s, budget)
+            sy = WaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
+                            legacy_records=False)
+            K = box.K
+        else:
+            if args.strong:   # the 1-GPU mesh, split over the ranks (needs nx >= world layers)
+                from paper_1512_06025_b200.mesh_device import BoxMesh
 
-                mesh_n[N] = fill_n(N)
-                mesh = cube_mesh_device(mesh_n[N])
-                torch.cuda.empty_cache()   # return the builder's scratch before the context allocates
-                K = mesh.K
-            Ks[N] = K
-            sy = make_system(N)
-            q = torch.randn((4, K, sy.Np), generator=gen, device="cuda", dtype=sy.torch_dtype)
-            q2, res = torch.empty_like(q), torch.randn_like(q)
-            dt = stable_dt(mesh, N, 1.0)
+                one = fill_box(N, s, budget)
+                box = BoxMesh(max(one.nx, world), one.ny, one.nz)
+            else:             # weak: an HBM-filling slab per rank
+                box = fill_box(N, s, budget, world)
+            sy = DistWaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
+                                rank, world, legacy_records=False)
+            K = sy.K
+        Ks[N] = K
+        q = torch.randn((4, K, np_of(N)), generator=gen, device="cuda", dtype=sy.torch_dtype)
+        q2, res = torch.empty_like(q), torch.randn_like(q)
+        dt = stable_dt(box, N, 1.0)
 
-            def stage():
-                sy.stage_into(q, q2, res, RK4A[1], RK4B[1], dt, args.lift)
+        def stage():
+            sy.stage_into(q, q2, res, RK4A[1], RK4B[1], dt, args.lift)
 
-            for _ in range(args.warmup):
-                stage()
-            torch.cuda.synchronize()
-            if world > 1:
-                torch.distributed.barrier()
-            tot = 0.0
-            for _ in range(args.steps):
-                flush.zero_()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                stage()
-                b.record()
-                b.synchronize()
-                tot += a.elapsed_time(b)
-            torch.cuda.synchronize()
-            per_n[N] = tot
-            t_stage = tot / args.steps
-            ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9   # K of this order's mesh
-            row = {"gdofs_stage": 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
-                   "stage_gbs": ach, "stage_frac": ach / peak}
-            if not args.quick and world == 1 and args.fill <= 0:
-                rhs = torch.empty_like(q)
-                reps = max(3, args.steps)
-                tv = time_launches(torch, lambda: sy.volume_into(q, rhs), flush, reps)
-                row["volume_ms"], row["volume_frac"] = tv, volume_bytes(N, s, K) / (tv * 1e-3) / 1e9 / peak
-                for mode in ("factorized", "optimal", "dense"):
-                    ts = time_launches(torch, lambda: sy.surface_into(q, rhs, mode), flush, reps)
-                    row[f"surface_{mode}_ms"] = ts
-                    row[f"surface_{mode}_frac"] = surface_bytes(N, s, K) / (ts * 1e-3) / 1e9 / peak
-                from paper_1512_06025_b200.solver import _device_update
-                tu = time_launches(torch, lambda: _device_update(q2, res, rhs, RK4A[1], RK4B[1], dt), flush, reps)
-                row["update_ms"], row["update_frac"] = tu, update_bytes(N, s, K) / (tu * 1e-3) / 1e9 / peak
-                row["unfused_gdofs"] = 4 * K * np_of(N) / ((tv + row["surface_optimal_ms"] + tu) * 1e-3) / 1e9
-                del rhs
-            # end to end through the public API with a pinned host state: H2D + 5 stages + D2H
-            # (N > 1: each rank's slab through DistWaveSystem.step_into, max over ranks)
-            if args.fill > 0:
-                rows[str(N)] = row
-                row["K"] = K
-                row["hbm_fraction"] = (12 * np_of(N) * s + 2 * 36 * s + 20) * K / torch.cuda.get_device_properties(
-                    dev).total_memory
-                del sy, q, q2, res
-                mesh = None
-                torch.cuda.empty_cache()
-                continue
-            host = torch.empty((4, K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
-            host.copy_(q)
-            reps = 2 if args.quick else max(2, min(args.steps, 5))
-            if world == 1:
-                st = FieldState(host.numpy(), "bernstein")
-                lsrk4_step(sy, st, dt, args.lift)   # warm
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                for _ in range(reps):
-                    lsrk4_step(sy, st, dt, args.lift)
-                torch.cuda.synchronize()
-                e2e = (time.perf_counter() - t0) * 1e3 / reps
-                del st
-            else:
-                qd, qt, rd = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
-
-                def e2e_step():
-                    qd.copy_(host, non_blocking=True)
-                    sy.step_into(qd, qt, rd, dt, args.lift)
-                    host.copy_(qd, non_blocking=True)
-                    torch.cuda.synchronize()
-
-                e2e_step()
-                torch.distributed.barrier()
-                t0 = time.perf_counter()
-                for _ in range(reps):
-                    e2e_step()
-                e2e = (time.perf_counter() - t0) * 1e3 / reps
-                tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
-                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-                e2e = float(tt.item())
-                del qd, qt, rd
-            row["e2e_ms_step"] = e2e
-            row["e2e_bytes"] = 2 * host.numel() * host.element_size()
-            del host
-            rows[str(N)] = row
-            del sy, q, q2, res
-            torch.cuda.empty_cache()
+        for _ in range(args.warmup):
+            stage()
+        t = events_time(torch, stage, args.steps, world > 1)
+        t = max_over_ranks(torch, t, world)
+        per_n[N] = t
+        t_stage = t / args.steps
+        ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9
+        row = {"K": K, "box": [box.nx, box.ny, box.nz], "hbm_fraction": resident_bytes(N, s, K) / total_mem,
+               "gdofs_stage": world * 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
+               "stage_gbs": ach, "stage_frac": ach / peak}
+        if world == 1 and not args.quick:
+            reps = max(3, args.steps // 2)
+            sy.volume_into(q, q2)
+            tv = events_time(torch, lambda: sy.volume_into(q, q2), reps) / reps
+            sy.surface_into(q, q2, args.lift)
+            ts = events_time(torch, lambda: sy.surface_into(q, q2, args.lift), reps) / reps
+            tu = events_time(torch, lambda: _device_update(q2, res, q, RK4A[1], RK4B[1], dt), reps) / reps
+            row.update(volume_ms=tv, volume_frac=volume_bytes(N, s, K) / (tv * 1e-3) / 1e9 / peak,
+                       surface_ms=ts, surface_frac=surface_bytes(N, s, K) / (ts * 1e-3) / 1e9 / peak,
+                       update_ms=tu, update_frac=update_bytes(N, s, K) / (tu * 1e-3) / 1e9 / peak,
+                       unfused_gdofs=4 * K * np_of(N) / ((tv + ts + tu) * 1e-3) / 1e9)
+        rows[str(N)] = row
+        del sy, q, q2, res
     total_ms = sum(per_n.values())
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-        torch.distributed.barrier()
-    dofs_per_step = sum(4 * Ks[N] * np_of(N) for N in orders)
-    value = world * dofs_per_step * args.steps / (total_ms * 1e-3) / 1e9
-    out = dict(per_order=rows, value=value, ms_per_step=total_ms / args.steps, clocks=clk.summary())
-    Nd = max(orders, key=lambda N: per_n[N])   # dominant kernel: the order with the largest stage time
+    dofs = sum(4 * Ks[N] * np_of(N) for N in orders)
+    value = world * dofs * args.steps / (total_ms * 1e-3) / 1e9
+    Nd = max(orders, key=lambda N: per_n[N])
     t_d = per_n[Nd] / args.steps
     ach = stage_bytes(Nd, s, Ks[Nd]) / (t_d * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(args.dtype, {}).get(f"n{args.n}", {}).get(str(Nd))
-    out["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                       "traffic": traffic, "kernel": f"opt_kernel<{args.dtype},N={Nd},OP_STAGE> ({args.lift} lift)",
-                       "peak_kind": peak_kind, "bytes_per_launch": stage_bytes(Nd, s, Ks[Nd])}
-    out["gpu_launches"] = args.steps * len(orders)
-    if args.fill > 0:
-        out["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                      "what": "not measured in --fill mode (a host copy of an HBM-filling state does not fit)"}
-        out["fill_meshes"] = {str(N): {"n": mesh_n[N], "K": Ks[N]} for N in orders}
-        return out, Ks[orders[-1]]
-    e2e_ms = sum(r["e2e_ms_step"] for r in rows.values())
-    e2e_dofs = sum(5 * 4 * K * np_of(N) for N in orders)
-    out["e2e"] = {"value": world * e2e_dofs / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-                  "h2d_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
-                  "d2h_bytes_per_step": world * sum(r["e2e_bytes"] // 2 for r in rows.values()),
-                  "what": ("lsrk4_step (5 fused stages) on a pinned numpy state per order: H2D + stages + D2H "
-                           "(chunk-pipelined through bbdg_step_host for states >= 32 MB: copies overlap stages)"
-                           if world == 1 else "per rank: pinned host slab H2D + DistWaveSystem.step_into (5 "
-                           "exchanged stages) + D2H, max over ranks")}
-    if world == 1 and args.nodal and not args.quick:
-        out["comparison"] = compare_bases(args, dtype, flush)
-    return out, K
+        tr = json.loads(tp.read_text()).get("fill", {}).get(dname, {}).get(str(Nd))
+        if tr and tr.get("K") == Ks[Nd]:
+            traffic = tr["dram_bytes"]
+    roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
+            "kernel": f"bbdg::opt_kernel<{'float' if s == 4 else 'double'}, {Nd}, 3 (OP_STAGE), FSR>",
+            "bytes_per_launch": stage_bytes(Nd, s, Ks[Nd]),
+            "bytes_model": "K ((16 Np + 16 Nfp + 36) s + 20): q in/out, res r/w, neighbour traces, geometry record, "
+                           "connectivity"}
+    return {"value": value, "ms_per_step": total_ms / args.steps, "per_order": rows, "roofline": roof,
+            "launches": args.steps * len(orders)}
 
 
-def compare_bases(args, dtype, flush):
-    """configs[1]: BB (fused stage / rhs) vs nodal DG rhs -- node-per-thread dense (paper NPT) and
-    block-partitioned tensor-core (paper EPT) -- on cube_mesh(26), per order."""
+def e2e_host(args, dname):
+    """lsrk4_step through the public API on a host numpy state (cube_mesh(e2e_n)): H2D + 5 stages + D2H,
+    per order, for a pinned and a pageable array."""
     import torch
 
-    from paper_1512_06025_b200 import cube_mesh
+    from paper_1512_06025_b200 import BernsteinRefOps, FieldState, Materials, WaveSystem, cube_mesh, lsrk4_step
+    from paper_1512_06025_b200 import stable_dt
+
+    dtype = np.float32 if dname == "f32" else np.float64
+    m = cube_mesh(args.e2e_n)
+    out = {"mesh": f"cube_mesh({args.e2e_n}) K={m.K}", "per_order": {}}
+    tot = {"pinned": 0.0, "pageable": 0.0}
+    dofs, nbytes = 0, 0
+    for N in parse_orders(args.orders):
+        sy = WaveSystem(m, BernsteinRefOps.build(N), Materials.homogeneous(m.K), dtype)
+        dt = stable_dt(m, N, 1.0)
+        pinned = torch.empty((4, m.K, sy.Np), dtype=sy.torch_dtype, pin_memory=True)
+        pinned.normal_()
+        page = pinned.numpy().copy()
+        row = {}
+        for kind, arr in (("pinned", pinned.numpy()), ("pageable", page)):
+            st = FieldState(arr, "bernstein")
+            lsrk4_step(sy, st, dt, args.lift)   # warm
+            torch.cuda.synchronize()
+            reps = 3
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                lsrk4_step(sy, st, dt, args.lift)   # returns with the host array updated
+            row[f"{kind}_ms_step"] = (time.perf_counter() - t0) * 1e3 / reps
+            tot[kind] += row[f"{kind}_ms_step"]
+        out["per_order"][str(N)] = row
+        dofs += 5 * 4 * m.K * sy.Np
+        nbytes += pinned.numel() * pinned.element_size()
+        del sy, pinned, page
+        torch.cuda.empty_cache()
+    out["value"] = dofs / (tot["pinned"] * 1e-3) / 1e9
+    out["pageable_value"] = dofs / (tot["pageable"] * 1e-3) / 1e9
+    out["bytes_per_step"] = nbytes
+    return out
+
+
+def compare_bases(args, dname):
+    """configs[1]: BB (fused stage / rhs, and the paper's non-optimal ELL and dense lifts) vs nodal
+    DG rhs -- node-per-thread dense (paper NPT) and block-partitioned tensor-core (paper EPT) -- on
+    cube_mesh(26), per order."""
+    import torch
+
+    from paper_1512_06025_b200 import BernsteinRefOps, Materials, NodalRefOps, WaveSystem, cube_mesh
     from paper_1512_06025_b200.solver import RK4A, RK4B
 
+    dtype = np.float32 if dname == "f32" else np.float64
     mesh = cube_mesh(26)
     out = {"mesh": f"cube_mesh(26) K={mesh.K}", "per_order": {}}
     for N in parse_orders(args.orders):
-        sb, sn = build_system(mesh, N, dtype), build_system(mesh, N, dtype, "nodal")
+        sb = WaveSystem(mesh, BernsteinRefOps.build(N), Materials.homogeneous(mesh.K), dtype)
+        sn = WaveSystem(mesh, NodalRefOps.build(N), Materials.homogeneous(mesh.K), dtype)
         q = torch.randn((4, mesh.K, sb.Np), device="cuda", dtype=sb.torch_dtype)
         q2, res, rhs = torch.empty_like(q), torch.randn_like(q), torch.empty_like(q)
         reps = 3
-        tb = time_launches(torch, lambda: sb.rhs_into(q, rhs, args.lift), flush, reps)
-        ts = time_launches(torch, lambda: sb.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, args.lift), flush, reps)
-        tn = time_launches(torch, lambda: sn.rhs_into(q, rhs, "dense"), flush, reps)
-        tk = time_launches(torch, lambda: sn.rhs_into(q, rhs, "blocked"), flush, reps)
+
+        def tm(fn):
+            fn()
+            return events_time(torch, fn, reps) / reps
+
+        tb = tm(lambda: sb.rhs_into(q, rhs, args.lift))
+        ts = tm(lambda: sb.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, args.lift))
+        te = tm(lambda: sb.surface_into(q, rhs, "ell"))
+        tdn = tm(lambda: sb.surface_into(q, rhs, "dense"))
+        tso = tm(lambda: sb.surface_into(q, rhs, args.lift))
+        tn = tm(lambda: sn.rhs_into(q, rhs, "dense"))
+        tk = tm(lambda: sn.rhs_into(q, rhs, "blocked"))
         flops = 2 * mesh.K * 4 * (3 * sb.Np ** 2 + sb.Np * 4 * sb.ops.Nfp)   # useful nodal GEMM flops
-        out["per_order"][str(N)] = {"bb_rhs_ms": tb, "bb_stage_ms": ts, "nodal_npt_rhs_ms": tn,
-                                    "nodal_blocked_rhs_ms": tk, "nodal_blocked_tflops": flops / tk / 1e9,
+        out["per_order"][str(N)] = {"bb_rhs_ms": tb, "bb_stage_ms": ts, "bb_surface_sweeps_ms": tso,
+                                    "bb_surface_ell_ms": te, "bb_surface_dense_ms": tdn,
+                                    "nodal_npt_rhs_ms": tn, "nodal_blocked_rhs_ms": tk,
+                                    "nodal_blocked_tflops": flops / tk / 1e9,
                                     "bb_over_nodal_npt": tn / tb, "bb_over_nodal_blocked": tk / tb}
         del sb, sn, q, q2, res, rhs
         torch.cuda.empty_cache()
     return out
 
 
-# ---------------------------------------------------------------------- CPU arm (oracle port)
-def cpu_sweep(orders, n, dtype, reps=1, lift="factorized", budget_s=None):
-    """Time one LSRK stage (rhs + update) per order with the oracle on cube_mesh(n)."""
+# ---------------------------------------------------------------------- CPU arm (the reference algorithm)
+_CPU = {}
+
+
+def _cpu_init():
+    try:   # one BLAS thread per worker process: the workers already cover the cores
+        from threadpoolctl import threadpool_limits
+
+        _CPU["limits"] = threadpool_limits(1)
+    except ImportError:
+        pass
+
+
+def _cpu_chunk(args):
+    N, lo, hi, mode = args
+    sy, q, res, dt = _CPU[N]
+    sy.stage(q, res, RK4A_1, RK4B_1, dt, mode, lo, hi)   # rows of [lo, hi): q_out, res_out (not shipped back)
+    return hi - lo
+
+
+RK4A_1 = -567301805773.0 / 1357537059087.0
+RK4B_1 = 5161836677717.0 / 13612068292357.0
+
+
+def cpu_sweep(orders, n, dtype, lifts=("optimal", "factorized"), procs=None, reps=1):
+    """One LSRK stage per order with the oracle port (the reference algorithm: gather + einsum
+    ELL rows, solver.py:139-214) on cube_mesh(n), element ranges split over `procs` forked
+    workers (one BLAS thread each).  Setup (tables, coordinate-matched trace maps) is built once,
+    before the workers fork, and is not timed.  Returns [{lift: (GDOF/s, seconds)}] per rep, K, procs."""
+    import multiprocessing as mp
+
     sys.path.insert(0, str(ROOT / "oracle"))
     import bbdg_oracle as orc
 
-    from paper_1512_06025_b200 import cube_mesh
+    from paper_1512_06025_b200 import cube_mesh, stable_dt
 
+    procs = procs or os.cpu_count() or 1
     m = cube_mesh(n)
     arrays = orc.mesh_arrays(m)
-    tot_t, tot_dofs = 0.0, 0
     rng = np.random.default_rng(2024)
     for N in orders:
         sy = orc.OracleSystem(arrays, orc.bernstein_tables(N), np.ones(m.K), np.ones(m.K), dtype)
-        q = rng.standard_normal((4, m.K, sy.t.Np)).astype(dtype)
-        res = np.zeros_like(q)
+        _CPU[N] = (sy, rng.standard_normal((4, m.K, sy.t.Np)).astype(dtype),
+                   rng.standard_normal((4, m.K, sy.t.Np)).astype(dtype), stable_dt(m, N, 1.0))
+    cuts = np.linspace(0, m.K, procs + 1).astype(int)
+    results = []
+    with mp.get_context("fork").Pool(procs, initializer=_cpu_init) as pool:
         for _ in range(reps):
-            t0 = time.perf_counter()
-            k = sy.rhs(q, lift)
-            res *= dtype(orc.RK4A[1])
-            res += dtype(1e-3) * k
-            q += dtype(orc.RK4B[1]) * res
-            tot_t += time.perf_counter() - t0
-            tot_dofs += 4 * m.K * sy.t.Np
-    return tot_dofs / tot_t / 1e9, m.K, tot_t
+            out = {}
+            for lift in lifts:
+                t_tot, dofs = 0.0, 0
+                for N in orders:
+                    t0 = time.perf_counter()
+                    pool.map(_cpu_chunk, [(N, int(a), int(b), lift) for a, b in zip(cuts[:-1], cuts[1:]) if b > a])
+                    t_tot += time.perf_counter() - t0
+                    dofs += 4 * m.K * np_of(N)
+                out[lift] = (dofs / t_tot / 1e9, t_tot)
+            results.append(out)
+    for N in orders:
+        _CPU.pop(N, None)
+    return results, m.K, procs
 
 
+def cpu_sample_text(orders, n, K, lift, t, procs):
+    return (f"oracle port of the reference algorithm (numpy gather + einsum, solver.py:139-214), one LSRK stage "
+            f"per order N={orders} on cube_mesh({n}) (K={K}), {lift} lift, element ranges over {procs} processes, "
+            f"{t:.1f} s")
+
+
+# ---------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--n", type=int, default=40, help="cube_mesh(n): K = 6 n^3 per GPU")
+    ap.add_argument("--dtypes", default="f32,f64", help="first = the headline value")
     ap.add_argument("--orders", default="1-9")
-    ap.add_argument("--lift", default="optimal", choices=["optimal", "factorized", "dense"])
+    ap.add_argument("--lift", default="optimal", choices=["optimal", "factorized"])
+    ap.add_argument("--fill", type=float, default=0.8, help="fraction of free device memory per order")
+    ap.add_argument("--strong", action="store_true", help="N>1: split the 1-GPU mesh (default: weak scaling)")
+    ap.add_argument("--quick", action="store_true", help="stage sweep only (no breakdown, e2e, comparison)")
+    ap.add_argument("--e2e-n", type=int, default=40)
     ap.add_argument("--cpu-n", type=int, default=16, help="oracle sample mesh cube_mesh(cpu_n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-nodal", dest="nodal", action="store_false", help="skip the nodal NPT comparison")
-    ap.add_argument("--quick", action="store_true", help="skip the per-kernel breakdown")
-    ap.add_argument("--fill", type=float, default=0.0,
-                    help="configs[2] HBM-filling sweep: per order a cube_mesh (built on the GPU) whose q, q_out, res "
-                         "use this fraction of device memory (1 GPU; no breakdown / e2e)")
+    ap.add_argument("--no-nodal", dest="nodal", action="store_false")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    dnames = args.dtypes.split(",")
     orders = parse_orders(args.orders)
-    dtype = np.float32 if args.dtype == "f32" else np.float64
-    config = {"workload": f"BB-DG acoustic LSRK4 stage sweep N={args.orders}, cube_mesh({args.n}) K={6 * args.n ** 3}"
-                          f"{' per GPU (box of ' + str(world) + ' slabs)' if world > 1 else ''}, "
-                          f"{args.lift} lift", "K": 6 * args.n ** 3, "orders": orders, "lift": args.lift,
-              "l2": "flushed (256 MB write) before every timed launch", "materials": "homogeneous",
-              "parallelism": f"element slabs x{world}, NCCL face-trace halo" if world > 1 else "1 GPU"}
+    head = dnames[0]
+    scaling = "strong" if (args.strong and world > 1) else "weak"
+    config = {"workload": WORKLOAD.format(orders=args.orders, lift=args.lift), "orders": orders, "lift": args.lift,
+              "mesh": f"per order a device-built Kuhn box filling {args.fill:.2f} of free HBM"
+                      + (f" per rank (x-layer slabs, {scaling} scaling)" if world > 1 else ""),
+              "l2": "not flushed: every launch streams >= 1.4 GB (inputs larger than the 126 MB L2)",
+              "materials": "homogeneous (kappa = rho = 1)",
+              "parallelism": f"{world} GPUs: element slabs, NCCL face-trace halo" if world > 1 else "1 GPU"}
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": head,
+            "data": "synthetic (standard normal, seed 2024)", "config": config}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        ncores = os.cpu_count() or 1
-        os.environ.setdefault("OMP_NUM_THREADS", str(ncores))
-        vals = []
-        for _ in range(args.warmup if args.warmup < 1 else 1):
-            cpu_sweep(orders, max(2, args.cpu_n // 2), dtype)
-        for _ in range(args.steps):
-            v, Ks, _ = cpu_sweep(orders, args.cpu_n, dtype)
-            vals.append(v)
-        v = float(np.mean(vals))
-        sample = f"one LSRK stage per order N={args.orders} on cube_mesh({args.cpu_n}) (K={Ks}), factorized lift"
-        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-                          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-                          "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (standard normal, seed 2024)",
-                          "config": config,
-                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncores, "kind": "port",
-                                           "sample": sample},
-                          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        dtype = np.float32 if head == "f32" else np.float64
+        reps, K, procs = cpu_sweep(orders, args.cpu_n, dtype, lifts=(args.lift,), reps=args.warmup + args.steps)
+        timed = [r[args.lift] for r in reps[args.warmup:]]   # the first `warmup` sweeps warm the workers
+        v = float(np.mean([x[0] for x in timed]))
+        res = {args.lift: (v, float(np.mean([x[1] for x in timed])))}
+        sample = cpu_sample_text(args.orders, args.cpu_n, K, args.lift, res[args.lift][1], procs)
+        print(json.dumps(dict(base, impl="reference", value=v, ms_per_step=None,
+                              cpu_baseline={"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+                                            "sample": sample},
+                              e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})))
         return
 
     import torch
 
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.distributed.init_process_group("nccl")
-    out, K = run_ours(args, rank, world)
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
-    line = {"metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": out["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (standard normal, seed 2024)",
-            "config": config, "roofline": out["roofline"], "e2e": out["e2e"], "gpu_launches": out["gpu_launches"],
-            "clocks": out["clocks"], "per_order": out["per_order"]}
-    if args.fill > 0:
-        line["config"]["workload"] = (f"BB-DG acoustic LSRK4 stage sweep N={args.orders}, HBM-filling cube meshes "
-                                      f"({args.fill:.2f} of device memory for q, q_out, res), built on the GPU")
-        line["config"]["K"] = {N: v["K"] for N, v in out["fill_meshes"].items()}
-        line["config"]["fill"] = out["fill_meshes"]
-    if "comparison" in out:
-        line["comparison"] = out["comparison"]
-    if not args.no_cpu_baseline:
-        v, Ks, t = cpu_sweep(orders, args.cpu_n, dtype)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"oracle port, one LSRK stage per order N={args.orders} on "
-                                          f"cube_mesh({args.cpu_n}) (K={Ks}), factorized lift, {t:.1f} s"}
-    print(json.dumps(line))
+    dev = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    peak, peak_kind = load_peaks()
+    per_dtype = {}
+    with Clocks(dev) as clk:
+        for d in dnames:
+            per_dtype[d] = run_dtype(args, d, rank, world, dev, peak, clk)
+    line = dict(base, value=per_dtype[head]["value"], ms_per_step=per_dtype[head]["ms_per_step"],
+                roofline=dict(per_dtype[head]["roofline"], peak_kind=peak_kind),
+                gpu_launches=sum(r["launches"] for r in per_dtype.values()), clocks=clk.summary(),
+                per_order=per_dtype[head]["per_order"],
+                per_dtype={d: {"value": r["value"], "ms_per_step": r["ms_per_step"], "roofline": r["roofline"],
+                               "per_order": r["per_order"]} for d, r in per_dtype.items()})
+    if world > 1:
+        line["nccl"] = {"backend": "nccl", "nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version()))}
+    if world == 1 and not args.quick:
+        e2e = e2e_host(args, head)
+        line["e2e"] = {"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["bytes_per_step"],
+                       "d2h_bytes_per_step": e2e["bytes_per_step"], "pageable_value": e2e["pageable_value"],
+                       "what": f"lsrk4_step (5 fused stages) on a host numpy state per order, {e2e['mesh']}: H2D + "
+                               "stages + D2H in the timed region (pinned: chunk-pipelined bbdg_step_host; "
+                               "pageable_value: an ordinary numpy array)", "per_order": e2e["per_order"]}
+        if args.nodal:
+            line["comparison"] = compare_bases(args, head)
+    else:
+        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                       "what": "not measured in --quick / multi-GPU mode"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dtype = np.float32 if head == "f32" else np.float64
+        reps, K, procs = cpu_sweep(orders, args.cpu_n, dtype, lifts=(args.lift, "factorized"), reps=2)
+        res = reps[-1]
+        line["cpu_baseline"] = {"value": res[args.lift][0], "unit": UNIT, "cores": procs, "kind": "port",
+                                "sample": cpu_sample_text(args.orders, args.cpu_n, K, args.lift, res[args.lift][1],
+                                                          procs),
+                                "factorized_value": res["factorized"][0]}
+    if rank == 0:
+        print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
 

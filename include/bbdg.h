@@ -64,6 +64,17 @@ int bbdg_ctx_set_geometry(bbdg_ctx* ctx, const double* rst_dx, const double* kap
                           const double* normals, const double* face_scale, const double* tau_p,
                           const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code);
 
+/* The same per-element data for an axis-aligned box of nx x ny x nz cells, 6 Kuhn tetrahedra each
+ * (mesh.box_mesh / cube_mesh, reference mesh.py:95-155), computed on the device by closed-form
+ * index arithmetic -- no host arrays (HBM-filling meshes; slab-local setup of partitioned runs).
+ * The context holds the cell layers [cx0, cx1) (K = 6 (cx1 - cx0) ny nz, x-slab-major element
+ * order); faces into layers outside the slab but inside the box are halo faces whose slots follow
+ * partition.build_halo_plan's order.  Homogeneous materials kappa, rho.  legacy_records = 0 builds
+ * only the fused record of the hot-path kernels (the ELL, dense and nodal kernels then return
+ * BBDG_ERR_UNSUPPORTED).  Synchronises `stream` (setup call). */
+int bbdg_ctx_set_box_mesh(bbdg_ctx* ctx, int nx, int ny, int nz, int cx0, int cx1, const double* lo, const double* hi,
+                          double kappa, double rho, int legacy_records, void* stream);
+
 /* Lift tables (host, float64): E_L as ELL (Np, width) for the "factorized"
  * mode (bernstein.py:273-310) and the dense (Np, 4 Nfp) lift for "dense"
  * (bernstein.py:332-347, nodal.py:411-419).  Either pointer may be NULL. */
@@ -164,6 +175,7 @@ int bbdg_dense_apply(int dtype, int64_t nb, int nrows, int ncols, const void* A,
                      void* stream);
 
 /* Introspection used by tests and the benchmark. */
+int bbdg_ctx_read_records(bbdg_ctx* ctx, void* geo, int32_t* nbr, int32_t* code);
 int bbdg_tile_elems(int N, int dtype);
 int64_t bbdg_kernel_smem(int N, int dtype, int op, int lift, int basis);
 

@@ -48,7 +48,7 @@ def _sources_digest() -> str:
 
 def _units():
     units = [("bbdg_capi", CSRC / "bbdg_capi.cu", []), ("bbdg_func", CSRC / "bbdg_func.cu", []),
-             ("bbdg_ops", CSRC / "bbdg_ops.cu", [])]
+             ("bbdg_ops", CSRC / "bbdg_ops.cu", []), ("bbdg_mesh", CSRC / "bbdg_mesh.cu", [])]
     for tname, t in (("f32", "float"), ("f64", "double")):
         for n in range(1, MAX_DEGREE + 1):
             units.append((f"k_{tname}_{n}", CSRC / "bbdg_kernels.cu",

@@ -6,31 +6,10 @@
 #include <vector>
 
 #include "bbdg_common.cuh"
+#include "bbdg_geo.cuh"
 #include "bbdg_internal.h"
 #include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
-
-struct bbdg_ctx {
-  int N, basis, dtype;
-  int64_t K;
-  int Np, Nfp;
-  int num_sms;
-  void* geo_vol = nullptr;   // T (K,12)
-  void* geo_surf = nullptr;  // T (K,24)
-  void* geo = nullptr;       // T (K,36) fused record of the optimal-lift kernels (kGeoRec)
-  int32_t* nbr = nullptr;    // (K,4)
-  int32_t* code = nullptr;   // (K)
-  void* el_vals = nullptr;   // T (Np,w)
-  uint16_t* el_cols = nullptr;
-  int el_w = 0;
-  void* liftT = nullptr;     // T (4Nfp,Np)
-  void* dT = nullptr;        // T (3,Np,Np)
-  void* bvol = nullptr;      // nodal blocked: D_m^T MMA fragments
-  void* blift = nullptr;     // nodal blocked: L^T MMA fragments
-  void* flux = nullptr;      // nodal blocked: (4, K, 4 Nfp) face-flux scratch
-  const void* halo = nullptr;
-  int64_t nhalo = 0;
-};
 
 namespace bbdg {
 
@@ -64,6 +43,16 @@ static KernelEntry lookup(int dtype, int N, int op, int lift, int basis) {
   return KernelEntry{nullptr, nullptr, 0};
 }
 
+void free_geometry(bbdg_ctx* c) {
+  cudaFree(c->geo_vol);
+  cudaFree(c->geo_surf);
+  cudaFree(c->geo);
+  cudaFree(c->nbr);
+  cudaFree(c->code);
+  c->geo_vol = c->geo_surf = c->geo = nullptr;
+  c->nbr = c->code = nullptr;
+}
+
 template <typename T> static void* upload(const std::vector<T>& h, int* rc) {
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, std::max<size_t>(h.size(), 1) * sizeof(T));
@@ -87,44 +76,22 @@ static int set_geometry_t(bbdg_ctx* c, const double* rst_dx, const double* kappa
                           const double* normals, const double* face_scale, const double* tau_p,
                           const double* tau_u, const int32_t* nbr_elem, const int8_t* nbr_code) {
   const int64_t K = c->K;
-  std::vector<T> gv((size_t)K * kGeoVol, T(0)), gs((size_t)K * kGeoSurf), gr((size_t)K * kGeoRec, T(0));
+  std::vector<T> gv((size_t)K * kGeoVol), gs((size_t)K * kGeoSurf), gr((size_t)K * kGeoRec);
   std::vector<int32_t> nb((size_t)K * 4), cd((size_t)K);
   for (int64_t k = 0; k < K; ++k) {
-    for (int j = 0; j < 9; ++j) gv[k * kGeoVol + j] = static_cast<T>(rst_dx[k * 9 + j]);
-    gv[k * kGeoVol + 9] = static_cast<T>(kappa[k]);
-    gv[k * kGeoVol + 10] = static_cast<T>(inv_rho[k]);
-    T* r = &gr[k * kGeoRec];
-    r[24] = static_cast<T>(kappa[k]);
-    r[25] = static_cast<T>(inv_rho[k]);
-    for (int j = 0; j < 9; ++j) r[26 + j] = static_cast<T>(rst_dx[k * 9 + j]);
-    uint32_t packed = 0;
+    int code[4];
     for (int f = 0; f < 4; ++f) {
-      T* g = &gs[k * kGeoSurf + f * 6];
-      for (int i = 0; i < 3; ++i) g[i] = static_cast<T>(normals[(k * 4 + f) * 3 + i]);
-      g[3] = static_cast<T>(face_scale[k * 4 + f]);
-      g[4] = static_cast<T>(tau_p[k * 4 + f]);
-      g[5] = static_cast<T>(tau_u[k * 4 + f]);
+      code[f] = static_cast<uint8_t>(nbr_code[k * 4 + f]);
       const int32_t n = nbr_elem[k * 4 + f];
-      const int code = static_cast<uint8_t>(nbr_code[k * 4 + f]);
-      const bool halo = (code >> 6) & 1, bnd = (code >> 5) & 1;
-      // fused record: the boundary mirror (jp = -2 p-, solver.py:173) rides on the sign of Bs
-      const double hs = 0.5 * face_scale[k * 4 + f];
-      for (int i = 0; i < 3; ++i) r[4 * f + i] = static_cast<T>(normals[(k * 4 + f) * 3 + i]);
-      r[4 * f + 3] = static_cast<T>(bnd ? -hs : hs);
-      r[16 + 2 * f] = static_cast<T>(tau_p[k * 4 + f]);
-      r[17 + 2 * f] = static_cast<T>(hs * tau_u[k * 4 + f]);
+      const bool halo = (code[f] >> 6) & 1, bnd = (code[f] >> 5) & 1;
       if (!bnd && !halo && (n < 0 || n >= K)) return set_error(BBDG_ERR_ARG, "neighbour element out of range");
-      nb[k * 4 + f] = n;
-      packed |= static_cast<uint32_t>(code) << (8 * f);
     }
-    cd[k] = static_cast<int32_t>(packed);
+    pack_element<T>(rst_dx + k * 9, kappa[k], inv_rho[k], normals + k * 12, face_scale + k * 4, tau_p + k * 4,
+                    tau_u + k * 4, nbr_elem + k * 4, code, &gr[k * kGeoRec], &gv[k * kGeoVol], &gs[k * kGeoSurf],
+                    &nb[k * 4], &cd[k]);
   }
   int rc = BBDG_OK;
-  cudaFree(c->geo_vol);
-  cudaFree(c->geo_surf);
-  cudaFree(c->nbr);
-  cudaFree(c->code);
-  cudaFree(c->geo);
+  free_geometry(c);
   c->geo = upload(gr, &rc);
   c->geo_vol = upload(gv, &rc);
   c->geo_surf = upload(gs, &rc);
@@ -292,7 +259,7 @@ using namespace bbdg;
 
 static int check_ctx(const bbdg_ctx* c) {
   if (!c) return set_error(BBDG_ERR_ARG, "null context");
-  if (!c->geo_vol) return set_error(BBDG_ERR_UNSUPPORTED, "geometry not uploaded (bbdg_ctx_set_geometry)");
+  if (!c->geo) return set_error(BBDG_ERR_UNSUPPORTED, "geometry not uploaded (bbdg_ctx_set_geometry)");
   return BBDG_OK;
 }
 
@@ -315,6 +282,7 @@ static int internal_lift(int ext) {
 // validates the external lift id and turns it into the kernel family
 static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
   if (c->basis == BBDG_BASIS_NODAL) {
+    if (!c->geo_vol) return set_error(BBDG_ERR_UNSUPPORTED, "nodal kernels need the legacy geometry records");
     // WaveSystem forces "dense" for the nodal basis (solver.py:168-169); BLOCKED selects the
     // tensor-core (EPT) kernels for the same arithmetic
     if (lift == BBDG_LIFT_BLOCKED) {
@@ -336,6 +304,9 @@ static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
   if (surf && lift == BBDG_LIFT_DENSE && !c->liftT)
     return set_error(BBDG_ERR_UNSUPPORTED, "dense lift not uploaded (bbdg_ctx_set_lift_tables)");
   lift = internal_lift(lift);
+  if (surf && lift != LIFT_OPTIMAL && !c->geo_vol)
+    return set_error(BBDG_ERR_UNSUPPORTED, "this lift mode needs the legacy geometry records (box context built "
+                                           "with the fused record only)");
   return BBDG_OK;
 }
 
@@ -380,11 +351,7 @@ int bbdg_ctx_create(int N, int basis, int dtype, int64_t K, bbdg_ctx** out) {
 
 void bbdg_ctx_destroy(bbdg_ctx* c) {
   if (!c) return;
-  cudaFree(c->geo_vol);
-  cudaFree(c->geo_surf);
-  cudaFree(c->geo);
-  cudaFree(c->nbr);
-  cudaFree(c->code);
+  free_geometry(c);
   cudaFree(c->el_vals);
   cudaFree(c->el_cols);
   cudaFree(c->liftT);

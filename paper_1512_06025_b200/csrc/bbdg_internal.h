@@ -8,12 +8,36 @@
 
 #include "../../include/bbdg.h"
 
+// One (mesh, degree, basis, dtype) context: immutable device tables after setup.
+struct bbdg_ctx {
+  int N, basis, dtype;
+  int64_t K;
+  int Np, Nfp;
+  int num_sms;
+  void* geo_vol = nullptr;   // T (K,12)  legacy records (tile / ELL / dense / nodal kernels); NULL when a
+  void* geo_surf = nullptr;  // T (K,24)  box context was built with the fused record only
+  void* geo = nullptr;       // T (K,36) fused record of the optimal-lift kernels (kGeoRec)
+  int32_t* nbr = nullptr;    // (K,4)
+  int32_t* code = nullptr;   // (K)
+  void* el_vals = nullptr;   // T (Np,w)
+  uint16_t* el_cols = nullptr;
+  int el_w = 0;
+  void* liftT = nullptr;     // T (4Nfp,Np)
+  void* dT = nullptr;        // T (3,Np,Np)
+  void* bvol = nullptr;      // nodal blocked: D_m^T MMA fragments
+  void* blift = nullptr;     // nodal blocked: L^T MMA fragments
+  void* flux = nullptr;      // nodal blocked: (4, K, 4 Nfp) face-flux scratch
+  const void* halo = nullptr;
+  int64_t nhalo = 0;
+};
+
 namespace bbdg {
 
 constexpr int kMaxDegree = 9;
 
 int set_error(int code, const char* msg);
 int set_cuda_error(cudaError_t e, const char* where);
+void free_geometry(bbdg_ctx* c);
 
 struct KernelEntry {
   int (*launch)(const void* params, cudaStream_t stream, int num_sms);

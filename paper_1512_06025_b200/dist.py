@@ -22,12 +22,26 @@ from .solver import RK4A, RK4B, WaveSystem
 
 
 class DistWaveSystem:
-    def __init__(self, mesh, ops, materials, dtype=np.float64, rank=0, world=1, dist=None, align=1):
+    """One rank's slab.  `mesh` is a host Mesh (the rank keeps its element range) or a
+    mesh_device.BoxMesh, in which case the rank builds only its own x-layer slab on its device
+    (bbdg_ctx_set_box_mesh) and derives the halo plan in closed form -- no whole-mesh arrays
+    anywhere, so 8 x HBM-filling meshes set up in milliseconds."""
+
+    def __init__(self, mesh, ops, materials, dtype=np.float64, rank=0, world=1, dist=None, align=1,
+                 legacy_records=None):
         import torch
 
-        ranges = slab_ranges(mesh.K, world, align)
-        self.plan = build_halo_plan(mesh, world, rank, ranges)
-        self.local = WaveSystem(mesh, ops, materials, dtype, _plan=self.plan)
+        from .mesh_device import BoxMesh
+        from .partition import box_halo_plan
+
+        if isinstance(mesh, BoxMesh):
+            self.plan = box_halo_plan(mesh, world, rank)
+            self.local = WaveSystem(mesh.slab(rank, world), ops, materials, dtype, _plan=self.plan,
+                                    legacy_records=legacy_records)
+        else:
+            ranges = slab_ranges(mesh.K, world, align)
+            self.plan = build_halo_plan(mesh, world, rank, ranges)
+            self.local = WaveSystem(mesh, ops, materials, dtype, _plan=self.plan)
         self.torch = torch
         self.ex = HaloExchanger(self.plan, self.local.ops.Nfp, self.local.torch_dtype, "cuda",
                                 self.local.halo_pack, dist)
@@ -37,6 +51,14 @@ class DistWaveSystem:
     @property
     def K(self):
         return self.plan.n_local
+
+    @property
+    def Np(self):
+        return self.local.Np
+
+    @property
+    def torch_dtype(self):
+        return self.local.torch_dtype
 
     def empty_state(self):
         return self.local.empty_state()
@@ -54,10 +76,12 @@ class DistWaveSystem:
         for k0, k1 in self.halo_ranges:
             self.local.stage_range_into(q_in, q_out, res, a, b, dt, lift_mode, k0, k1)
 
-    def step_into(self, q, q_tmp, res, dt, lift_mode="optimal"):
-        """lsrk4_step on the slab: five exchanged stages, result left in q."""
+    def step_into(self, q, q_tmp, res, dt, lift_mode="optimal", q_tmp2=None):
+        """lsrk4_step on the slab: five exchanged stages, result left in q (with q_tmp2 the fifth
+        stage writes q directly, else one device copy)."""
         res.zero_()
-        bufs = [q, q_tmp]
+        seq = [q, q_tmp, q_tmp2, q_tmp, q_tmp2, q] if q_tmp2 is not None else [q, q_tmp, q, q_tmp, q, q_tmp]
         for s in range(5):
-            self.stage_into(bufs[s & 1], bufs[(s + 1) & 1], res, RK4A[s], RK4B[s], dt, lift_mode)
-        q.copy_(q_tmp)
+            self.stage_into(seq[s], seq[s + 1], res, RK4A[s], RK4B[s], dt, lift_mode)
+        if q_tmp2 is None:
+            q.copy_(q_tmp)

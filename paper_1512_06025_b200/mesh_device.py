@@ -108,3 +108,73 @@ def box_mesh_device(nx: int, ny: int, nz: int, lo=(-0.5, -0.5, -0.5), hi=(0.5, 0
 
 def cube_mesh_device(n: int, lo=(-0.5, -0.5, -0.5), hi=(0.5, 0.5, 0.5), device="cuda") -> Mesh:
     return box_mesh_device(n, n, n, lo, hi, device)
+
+
+class BoxMesh:
+    """A box of nx x ny x nz cells, 6 Kuhn tets each, that is never materialised on the host:
+    ``WaveSystem`` expands it on the device with ``bbdg_ctx_set_box_mesh`` (closed-form index
+    arithmetic, one thread per element).  Same elements, order, connectivity and geometry as
+    ``mesh.box_mesh`` / ``cube_mesh`` (reference mesh.py:127-155).  ``slab(rank, world)`` is the
+    rank's contiguous range of x cell layers (x-slab-major element order), so every rank of a
+    partitioned run builds only its own elements.
+
+    Exposes the ``Mesh`` attributes the time stepper needs (``K``, ``h_min``, ``h_max``,
+    ``volume``); ``to_mesh()`` materialises the full host mesh (small boxes: tests, functionals).
+    """
+
+    def __init__(self, nx: int, ny: int, nz: int, lo=(-0.5, -0.5, -0.5), hi=(0.5, 0.5, 0.5), cx0: int = 0,
+                 cx1: int | None = None):
+        if min(nx, ny, nz) < 1:
+            raise ValueError("need at least one cell per axis")
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.lo = tuple(float(x) for x in lo)
+        self.hi = tuple(float(x) for x in hi)
+        self.cx0 = int(cx0)
+        self.cx1 = self.nx if cx1 is None else int(cx1)
+        if not 0 <= self.cx0 < self.cx1 <= self.nx:
+            raise ValueError("slab layers must satisfy 0 <= cx0 < cx1 <= nx")
+        # every cell is the same box: the 6 tets of one cell give the exact h range
+        from .mesh import box_mesh
+
+        step = [(h - l) / n for l, h, n in zip(self.lo, self.hi, (self.nx, self.ny, self.nz))]
+        cell = box_mesh(1, 1, 1, lo=(0.0, 0.0, 0.0), hi=tuple(step))
+        self.h_min, self.h_max = cell.h_min, cell.h_max
+        self.cell_jac = float(cell.jac[0])   # every Kuhn tet of a box has the same volume
+
+    @classmethod
+    def cube(cls, n: int, lo=(-0.5, -0.5, -0.5), hi=(0.5, 0.5, 0.5)) -> "BoxMesh":
+        return cls(n, n, n, lo, hi)
+
+    @property
+    def K(self) -> int:
+        """Elements of this slab (the whole box unless sliced)."""
+        return 6 * (self.cx1 - self.cx0) * self.ny * self.nz
+
+    @property
+    def K_total(self) -> int:
+        return 6 * self.nx * self.ny * self.nz
+
+    @property
+    def k0(self) -> int:
+        return 6 * self.cx0 * self.ny * self.nz
+
+    @property
+    def volume(self) -> float:
+        return float(np.prod(np.subtract(self.hi, self.lo)))
+
+    def slab_layers(self, rank: int, world: int) -> tuple[int, int]:
+        if not 1 <= world <= self.nx:
+            raise ValueError("need 1 <= world <= nx cell layers")
+        return (self.nx * rank) // world, (self.nx * (rank + 1)) // world
+
+    def slab(self, rank: int, world: int) -> "BoxMesh":
+        a, b = self.slab_layers(rank, world)
+        return BoxMesh(self.nx, self.ny, self.nz, self.lo, self.hi, a, b)
+
+    def to_mesh(self) -> Mesh:
+        from .mesh import box_mesh
+
+        return box_mesh(self.nx, self.ny, self.nz, self.lo, self.hi)
+
+    def __repr__(self):
+        return (f"BoxMesh({self.nx}x{self.ny}x{self.nz} cells, layers [{self.cx0}, {self.cx1}), K={self.K})")

@@ -128,8 +128,12 @@ def pack_traces_reference(q: np.ndarray, faces: np.ndarray, trace: np.ndarray) -
 
 
 class HaloExchanger:
-    """Posts one stage's face-trace exchange through torch.distributed (NCCL on the
-    GPU path, gloo in the CPU tests).  `packer(q, faces, out)` fills a send buffer."""
+    """Posts one stage's face-trace exchange through torch.distributed (NCCL on the GPU path,
+    gloo in the CPU tests): ONE send and ONE receive per peer and direction -- the packed
+    (4, n, Nfp) trace block -- grouped in a single batch_isend_irecv.  `packer(q, faces, out)`
+    fills a send buffer; `wait` completes the receives and scatters each peer's block into its
+    slots of the (4, nhalo, Nfp) halo array the kernels read.  All four fields travel so the
+    receiver's flux arithmetic is exactly the single-domain one (bitwise partition invariance)."""
 
     def __init__(self, plan: HaloPlan, Nfp: int, dtype, device, packer, dist=None):
         import torch
@@ -142,6 +146,8 @@ class HaloExchanger:
         self.send_faces = {r: torch.as_tensor(f, device=device) for r, f in plan.send.items()}
         self.send_bufs = {r: torch.empty((4, len(f), Nfp), dtype=dtype, device=device)
                           for r, f in plan.send.items()}
+        self.recv_bufs = {r: torch.empty((4, n, Nfp), dtype=dtype, device=device)
+                          for r, n in plan.recv_count.items()}
 
     def post(self, q):
         """Pack and post all sends/receives; returns the requests (wait() before use)."""
@@ -151,17 +157,56 @@ class HaloExchanger:
             self.packer(q, faces, self.send_bufs[r])
         for r in sorted(set(self.plan.recv_count) | set(self.send_faces)):
             if r in self.send_faces:
-                for F in range(4):
-                    ops.append(P2POp(self.dist.isend, self.send_bufs[r][F], r))
-            if r in self.plan.recv_count:
-                o, n = self.plan.recv_offset[r], self.plan.recv_count[r]
-                for F in range(4):
-                    ops.append(P2POp(self.dist.irecv, self.recv[F, o:o + n], r))
+                ops.append(P2POp(self.dist.isend, self.send_bufs[r], r))
+            if r in self.recv_bufs:
+                ops.append(P2POp(self.dist.irecv, self.recv_bufs[r], r))
         if not ops:
             return []
         return self.dist.batch_isend_irecv(ops)
 
-    @staticmethod
-    def wait(reqs):
+    def wait(self, reqs):
         for r in reqs:
             r.wait()
+        for r, buf in self.recv_bufs.items():
+            o, n = self.plan.recv_offset[r], self.plan.recv_count[r]
+            self.recv[:, o:o + n].copy_(buf)
+
+
+def box_halo_plan(box, world: int, rank: int) -> HaloPlan:
+    """The HaloPlan of `rank` for the x-layer slab partition of a device-built box (mesh_device.
+    BoxMesh), in closed form -- the same slots and send lists build_halo_plan derives from a host
+    mesh, without one.  Per interface of ny nz cells, the cut faces are the face opposite path
+    vertex 3 of tets 3 and 5 of the slab's first layer (neighbour: layer - 1) and the face opposite
+    path vertex 0 of tets 0 and 1 of its last layer (neighbour: layer + 1); each such tet has one
+    cut face, so (receiver element, face) order is cell order, then tet.  ``nbr`` / ``code`` stay
+    None: bbdg_ctx_set_box_mesh computes the local connectivity on the device."""
+    a, b = box.slab_layers(rank, world)
+    plane = box.ny * box.nz
+    jk = np.arange(plane, dtype=np.int64)
+    owner = [box.slab_layers(r, world) for r in range(world)]
+
+    def owner_of(layer):
+        return next(r for r, (x0, x1) in enumerate(owner) if x0 <= layer < x1)
+
+    plan = HaloPlan(rank, world, 6 * a * plane, 6 * b * plane, None, None)
+    first = 6 * jk                                    # local elements of the first layer's cells
+    last = 6 * ((b - a - 1) * plane + jk)             # ... of the last layer's cells
+    slot, halo = 0, []
+    if a > 0:
+        left = owner_of(a - 1)
+        plan.recv_offset[left], plan.recv_count[left] = slot, 2 * plane
+        slot += 2 * plane
+        halo.append(np.stack([first + 3, first + 5], 1).ravel())
+        # the left peer receives (its last layer, tets 0 and 1, face 0) <- mine (tets 3 and 5, face 3)
+        plan.send[left] = np.stack([np.stack([first + 3, first + 5], 1).ravel(),
+                                    np.full(2 * plane, 3)], 1).astype(np.int32)
+    if b < box.nx:
+        right = owner_of(b)
+        plan.recv_offset[right], plan.recv_count[right] = slot, 2 * plane
+        slot += 2 * plane
+        halo.append(np.stack([last, last + 1], 1).ravel())
+        plan.send[right] = np.stack([np.stack([last, last + 1], 1).ravel(), np.zeros(2 * plane, dtype=np.int64)],
+                                    1).astype(np.int32)
+    plan.nhalo = slot
+    plan.halo_elems = np.unique(np.concatenate(halo)) if halo else np.zeros(0, dtype=np.int64)
+    return plan

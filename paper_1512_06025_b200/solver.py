@@ -90,8 +90,12 @@ class FieldState:
 class WaveSystem:
     """Mesh + operators + materials bound to a device context (solver.py:96-193)."""
 
-    def __init__(self, mesh: Mesh, ops, materials: Materials, dtype=np.float64, _plan=None):
-        if len(materials.kappa) != mesh.K:
+    def __init__(self, mesh: Mesh, ops, materials: Materials, dtype=np.float64, _plan=None,
+                 legacy_records: bool | None = None):
+        from .mesh_device import BoxMesh
+
+        self._box = isinstance(mesh, BoxMesh)
+        if np.ndim(materials.kappa) != 0 and len(materials.kappa) != (mesh.K_total if self._box else mesh.K):
             raise ValueError("materials sized for a different mesh")
         self.mesh = mesh
         self._plan = _plan          # partition.HaloPlan for an element-partitioned rank
@@ -101,6 +105,19 @@ class WaveSystem:
             raise ValueError("dtype must be float32 or float64")
         self.ops = ops.astype(self.dtype)
         self.mat = materials
+        self._gather = None
+        if self._box:
+            # device-built box (bbdg_ctx_set_box_mesh): no per-element host arrays at all
+            kap, rho = np.asarray(materials.kappa, dtype=float), np.asarray(materials.rho, dtype=float)
+            if np.ptp(kap) != 0 or np.ptp(rho) != 0:
+                raise ValueError("a BoxMesh takes homogeneous materials")
+            self._box_mat = (float(kap.flat[0]), float(rho.flat[0]))
+            self._legacy = legacy_records if legacy_records is not None else mesh.K <= (1 << 22)
+            self._torch = _torch()
+            self._lib = _lib.load()
+            self._ctx = None
+            self._ctx = self._create_context(mesh, materials)
+            return
         K = mesh.K
         # per-face constants exactly as the reference forms them (solver.py:113-123)
         rc = materials.rho_c
@@ -122,7 +139,6 @@ class WaveSystem:
                 setattr(self, name, getattr(self, name)[sl])
             self._tau_p64, self._tau_u64, self._fscale64 = (self._tau_p64[sl], self._tau_u64[sl],
                                                             self._fscale64[sl])
-        self._gather = None
         self._torch = _torch()
         self._lib = _lib.load()
         self._ctx = None
@@ -134,6 +150,15 @@ class WaveSystem:
         ctx = C.c_void_p()
         _lib.check(L.bbdg_ctx_create(self.ops.N, _lib.BASIS[self.basis], _lib.DTYPE[np.dtype(self.dtype).name],
                                      self.K, C.byref(ctx)), "bbdg_ctx_create")
+        self._ctx = ctx   # owned from here on (released by __del__ if a later upload raises)
+        if self._box:
+            b = mesh
+            lo, hi = (C.c_double * 3)(*b.lo), (C.c_double * 3)(*b.hi)
+            _lib.check(L.bbdg_ctx_set_box_mesh(ctx, b.nx, b.ny, b.nz, b.cx0, b.cx1, lo, hi, self._box_mat[0],
+                                               self._box_mat[1], int(self._legacy), self._stream()),
+                       "bbdg_ctx_set_box_mesh")
+            self._upload_operators(ctx)
+            return ctx
         if self._plan is None:
             sl = slice(0, mesh.K)
             nbr, code = mesh.face_codes()
@@ -147,6 +172,11 @@ class WaveSystem:
         code = np.ascontiguousarray(code, dtype=np.int8)
         _lib.check(L.bbdg_ctx_set_geometry(ctx, *[a.ctypes.data for a in arrs], nbr.ctypes.data, code.ctypes.data),
                    "bbdg_ctx_set_geometry")
+        self._upload_operators(ctx)
+        return ctx
+
+    def _upload_operators(self, ctx):
+        L = self._lib
         if self.basis == "bernstein":
             cols, vals = self.ops_double.el_ell()
             dl = np.ascontiguousarray(self.ops_double.dense_L)
@@ -158,7 +188,6 @@ class WaveSystem:
             dl = np.ascontiguousarray(o.dense_L, dtype=np.float64)
             _lib.check(L.bbdg_ctx_set_nodal_ops(ctx, *[d.ctypes.data for d in D]), "bbdg_ctx_set_nodal_ops")
             _lib.check(L.bbdg_ctx_set_lift_tables(ctx, None, None, 0, dl.ctypes.data), "bbdg_ctx_set_lift_tables")
-        return ctx
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
@@ -173,7 +202,7 @@ class WaveSystem:
     @property
     def K(self) -> int:
         """Elements this system updates (the rank's slab for a partitioned system)."""
-        return self.mesh.K if self._plan is None else self._plan.n_local
+        return self.mesh.K if self._plan is None or self._box else self._plan.n_local
 
     @property
     def Np(self) -> int:
@@ -640,8 +669,13 @@ def discrete_energy(system: WaveSystem, state: FieldState) -> float:
         if d is None or d["M"].device != q.device:
             f64 = dict(dtype=torch.float64, device=q.device)
             sl = slice(None) if system._plan is None else slice(system._plan.k0, system._plan.k1)
-            jac = system.mesh.jac[sl]
-            coef = np.stack([jac / system.mat.kappa[sl]] + [jac * system.mat.rho[sl]] * 3)
+            if getattr(system, "_box", False):
+                jac = np.full(system.K, system.mesh.cell_jac)
+                kap, rho = system._box_mat
+            else:
+                jac = system.mesh.jac[sl]
+                kap, rho = system.mat.kappa[sl], system.mat.rho[sl]
+            coef = np.stack([jac / kap] + [jac * rho] * 3)
             d = dict(M=torch.as_tensor(np.array(M, dtype=np.float64), **f64),
                      coef=torch.as_tensor(np.ascontiguousarray(coef), **f64),
                      partial=torch.empty(q.shape[1], **f64), out=torch.empty(1, **f64))

@@ -88,7 +88,7 @@ def test_convergence_states_match_reference(N):
                    energy_guard=None)
     assert rel_l2(st.q.cpu().numpy(), g[f"q_N{N}"]) < 1e-12
     e, r = ErrorFunctional(m, sy.ops_double)(st), float(g[f"err_N{N}"])
-    assert abs(e - r) <= 1e-10 * r, (e, r)
+    assert abs(e - r) <= 1e-10 * r + 1e-15, (e, r)   # the functional's own cancellation: |p_h - p| << |p|
 
 
 def test_reference_divergence_reproduced(sens):

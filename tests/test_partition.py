@@ -73,7 +73,26 @@ def test_launch_ranges_cover_slab():
             assert inner[1] - inner[0] >= p.n_local // 4    # the middle slab overlaps the exchange
 
 
-def _gloo_worker(rank, world, port, out):
+@pytest.mark.parametrize("dims,world", [((4, 2, 3), 2), ((6, 3, 2), 3), ((5, 2, 2), 4), ((3, 1, 1), 3)])
+def test_box_halo_plan_matches_host_plan(dims, world):
+    """The closed-form plan of a device-built box slab (no host mesh) equals build_halo_plan's."""
+    from paper_1512_06025_b200.mesh_device import BoxMesh
+    from paper_1512_06025_b200.partition import box_halo_plan
+
+    box = BoxMesh(*dims)
+    m = box.to_mesh()
+    plane = dims[1] * dims[2]
+    ranges = [tuple(6 * x * plane for x in box.slab_layers(r, world)) for r in range(world)]
+    for r in range(world):
+        h, c = build_halo_plan(m, world, r, ranges), box_halo_plan(box, world, r)
+        assert (h.k0, h.k1, h.nhalo) == (c.k0, c.k1, c.nhalo)
+        assert h.recv_count == c.recv_count and h.recv_offset == c.recv_offset
+        assert set(h.send) == set(c.send) and all(np.array_equal(h.send[p], c.send[p]) for p in h.send)
+        assert np.array_equal(h.halo_elems, c.halo_elems)
+        assert c.launch_ranges() == h.launch_ranges()
+
+
+def _gloo_worker(rank, world, port, out, box_dims=None):
     import torch
     import torch.distributed as dist
 
@@ -81,17 +100,29 @@ def _gloo_worker(rank, world, port, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        m = msh.cube_mesh(3)
         N = 2
         ops = BernsteinRefOps.build(N)
+        if box_dims is None:
+            m = msh.cube_mesh(3)
+            plan = build_halo_plan(m, world, rank)
+            ex_plan = plan
+        else:   # exchange with the closed-form box plan, verify with the host mesh's plan
+            from paper_1512_06025_b200.mesh_device import BoxMesh
+            from paper_1512_06025_b200.partition import box_halo_plan
+
+            box = BoxMesh(*box_dims)
+            m = box.to_mesh()
+            plane = box.ny * box.nz
+            ranges = [tuple(6 * x * plane for x in box.slab_layers(r, world)) for r in range(world)]
+            plan = build_halo_plan(m, world, rank, ranges)
+            ex_plan = box_halo_plan(box, world, rank)
         q = np.random.default_rng(7).standard_normal((4, m.K, ops.Np))
-        plan = build_halo_plan(m, world, rank)
         trace = torch.as_tensor(ops.trace)
 
         def packer(qt, faces, outb):
             outb.copy_(qt[:, faces[:, 0].long()[:, None], trace[faces[:, 1].long()]])
 
-        ex = HaloExchanger(plan, ops.Nfp, torch.float64, "cpu", packer)
+        ex = HaloExchanger(ex_plan, ops.Nfp, torch.float64, "cpu", packer)
         ql = torch.as_tensor(q[:, plan.k0:plan.k1].copy())
         ex.wait(ex.post(ql))
         recv = ex.recv.numpy()
@@ -103,19 +134,22 @@ def _gloo_worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_gloo_two_rank_halo_exchange():
+@pytest.mark.parametrize("world,box_dims", [(2, None), (2, (4, 3, 2)), (3, (5, 2, 3))])
+def test_gloo_halo_exchange(world, box_dims):
+    """world-size 2/3 gloo runs of the one-message-per-peer exchange (host-mesh plan, and the
+    closed-form plan of a device-built box slab; the middle rank of 3 has two peers)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
-    port = 29500 + (os.getpid() % 1000)
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, out)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + 7 * world + (0 if box_dims is None else 3)
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, out, box_dims)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
-    assert dict(out) == {0: 1, 1: 1}
+    assert dict(out) == {r: 1 for r in range(world)}
 
 
 # ---------------------------------------------------------------------------- GPU

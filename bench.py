@@ -158,7 +158,7 @@ def fill_box(N, s, budget_bytes, ranks=1):
 def events_time(torch, fn, reps, sync_group=None):
     """Device time (ms) of `reps` back-to-back calls of fn, bracketed by barrier + synchronize."""
     torch.cuda.synchronize()
-    if sync_group is not None:
+    if sync_group:
         torch.distributed.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -166,7 +166,7 @@ def events_time(torch, fn, reps, sync_group=None):
         fn()
     b.record()
     torch.cuda.synchronize()
-    if sync_group is not None:
+    if sync_group:
         torch.distributed.barrier()
     return a.elapsed_time(b)
 

@@ -4,6 +4,7 @@
 #include <atomic>
 
 #include "bbdg_internal.h"
+#include "bbdg_ept.cuh"
 #include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
 
@@ -62,6 +63,35 @@ template <int OP, int FSR> int launch_opt(const void* vp, cudaStream_t stream, i
       opt_kernel<T, BBDG_N, OP, FSR>, cache, vp, stream, num_sms);
 }
 
+#ifndef BBDG_EPT_MAX_N
+#define BBDG_EPT_MAX_N 2   // element-per-thread register kernels for N <= this (bbdg_ept.cuh)
+#endif
+#ifndef BBDG_EPT_MAX_N64
+#define BBDG_EPT_MAX_N64 2
+#endif
+constexpr bool kEpt = BBDG_N <= (sizeof(BBDG_T) == 4 ? BBDG_EPT_MAX_N : BBDG_EPT_MAX_N64);
+
+// element-per-thread kernels: one warp per 32-element tile, W warps per CTA, one CTA per SM
+template <int OP, int NN = BBDG_N> int launch_ept(const void* vp, cudaStream_t stream, int num_sms) {
+  using T = BBDG_T;
+  using L = EptLayout<T, NN>;   // (dependent: only the orders that dispatch here instantiate it)
+  static DevCache attr;
+  auto kern = ept_kernel<T, NN, OP>;
+  const int dev = current_device();
+  if (attr[dev].load(std::memory_order_acquire) == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (ept)");
+    attr[dev].store(1, std::memory_order_release);
+  }
+  const Params<T>& p = *static_cast<const Params<T>*>(vp);
+  const int64_t ntiles = (p.kend - p.kbeg + L::KE - 1) / L::KE;
+  if (ntiles == 0) return BBDG_OK;
+  const int64_t grid = std::min<int64_t>((ntiles + L::W - 1) / L::W, (int64_t)num_sms);
+  kern<<<(unsigned)grid, L::threads, L::total, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "ept kernel launch");
+}
+
 // nodal block-partitioned path: flux kernel (surface ops), then the tensor-core GEMM kernel
 template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_sms) {
   using T = BBDG_T;
@@ -98,6 +128,10 @@ template <int OP, int LIFT, int BASIS> int launch(const void* vp, cudaStream_t s
     const Params<T>& p = *static_cast<const Params<T>*>(vp);
     constexpr int A = 16 / sizeof(T);
     const int fsr = (int)((p.K * Dims<BBDG_N>::Np) % A);
+    if constexpr (kEpt && (OP == OP_STAGE || OP == OP_RHS)) {
+      // 16-byte aligned field windows of every tile: the register kernel
+      if (fsr == 0 && (p.kbeg * Dims<BBDG_N>::Np) % A == 0) return launch_ept<OP>(vp, stream, num_sms);
+    }
     if constexpr (A == 4) {
       switch (fsr) {
         case 0: return launch_opt<OP, 0>(vp, stream, num_sms);

@@ -19,10 +19,10 @@ def _install_bbdg_shim():
     infrastructure; criteria 1-3, 6 and 9 of the acceptance suite (operator diagnostics, oplab)
     are out of scope and not copied."""
     import paper_1512_06025_b200 as pkg
-    from paper_1512_06025_b200 import bernstein, mesh, multiindex, nodal, quadrature, solver, sparse  # noqa: F401
+    from paper_1512_06025_b200 import bernstein, cli, mesh, multiindex, nodal, quadrature, solver, sparse  # noqa: F401
 
     sys.modules.setdefault("bbdg", pkg)
-    for name in ("bernstein", "mesh", "multiindex", "nodal", "quadrature", "solver", "sparse"):
+    for name in ("bernstein", "cli", "mesh", "multiindex", "nodal", "quadrature", "solver", "sparse"):
         sys.modules.setdefault(f"bbdg.{name}", getattr(pkg, name))
 
 

@@ -398,18 +398,27 @@ def host_chunk_plan(etoe, Np: int, itemsize: int, max_chunks: int = 48, min_stat
 
 def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -> bool:
     """Pipelined H2D + five stages + D2H of a pinned host state (bbdg_step_host); False if not applicable."""
-    if system._plan is not None or not isinstance(q_host, np.ndarray) or not q_host.flags.c_contiguous \
+    if system._plan is not None or system._box or not isinstance(q_host, np.ndarray) or not q_host.flags.c_contiguous \
             or not q_host.flags.writeable or q_host.dtype != np.dtype(system.dtype):
         return False
     torch = _torch()
+    registered = False
     if not torch.from_numpy(q_host).is_pinned():
-        return False   # pageable copies are synchronous: nothing would overlap
+        # an ordinary (pageable) numpy array: page-lock it for the duration of the step so the chunk
+        # copies are asynchronous and overlap the stages (pageable copies serialise with the kernels)
+        if q_host.nbytes < (32 << 20):
+            return False
+        if int(torch._C._cudart.cudaHostRegister(q_host.ctypes.data, q_host.nbytes, 0)) != 0:
+            return False   # registration refused: the plain copy path
+        registered = True
     if not hasattr(system, "_chunks"):
         etoe = system.mesh.etoe
         if _is_tensor(etoe):
             etoe = etoe.cpu().numpy()
         system._chunks = host_chunk_plan(etoe, system.ops.Np, np.dtype(system.dtype).itemsize)
     if system._chunks is None:
+        if registered:
+            torch._C._cudart.cudaHostUnregister(q_host.ctypes.data)
         return False
     bounds, reach = system._chunks
     if not hasattr(system, "_copy_streams"):
@@ -423,6 +432,8 @@ def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -
                                           int(reach), cs.cuda_stream, hs.cuda_stream, ds.cuda_stream),
                "bbdg_step_host")
     cs.synchronize()   # host_q holds the new state (reference: in place on return)
+    if registered:
+        torch._C._cudart.cudaHostUnregister(q_host.ctypes.data)
     return True
 
 

@@ -10,6 +10,7 @@
 #include "bbdg_internal.h"
 #include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
+#include "bbdg_tc.cuh"
 
 namespace bbdg {
 
@@ -403,8 +404,13 @@ int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* 
       const double* m[1] = {dense_L};
       cudaFree(c->blift);
       cudaFree(c->flux);
-      c->blift = c->dtype == BBDG_F32 ? upload(mma_fragments<float>(m, 1, Np, 4 * Nfp), &rc)
-                                      : upload(mma_fragments<double>(m, 1, Np, 4 * Nfp), &rc);
+      if (c->dtype == BBDG_F32) {   // tcgen05 operator images (bbdg_tc.cuh)
+        std::vector<float> vol, lift;
+        tc_operator_images(c->N, nullptr, dense_L, vol, lift, tf32_rna);
+        c->blift = upload(lift, &rc);
+      } else {
+        c->blift = upload(mma_fragments<double>(m, 1, Np, 4 * Nfp), &rc);
+      }
       const size_t fb = (size_t)4 * c->K * 4 * Nfp * (c->dtype == BBDG_F32 ? 4 : 8);
       cudaError_t e = cudaMalloc(&c->flux, std::max<size_t>(fb, 16));
       if (e != cudaSuccess) {
@@ -429,8 +435,13 @@ int bbdg_ctx_set_nodal_ops(bbdg_ctx* c, const double* Dr, const double* Ds, cons
   c->dT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
                                : upload(cast<double>(t.data(), t.size()), &rc);
   cudaFree(c->bvol);
-  c->bvol = c->dtype == BBDG_F32 ? upload(mma_fragments<float>(D, 3, Np, Np), &rc)
-                                 : upload(mma_fragments<double>(D, 3, Np, Np), &rc);
+  if (c->dtype == BBDG_F32) {   // tcgen05 operator images (bbdg_tc.cuh)
+    std::vector<float> vol, lift;
+    tc_operator_images(c->N, D, nullptr, vol, lift, tf32_rna);
+    c->bvol = upload(vol, &rc);
+  } else {
+    c->bvol = upload(mma_fragments<double>(D, 3, Np, Np), &rc);
+  }
   return rc;
 }
 

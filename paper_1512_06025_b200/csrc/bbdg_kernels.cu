@@ -7,6 +7,7 @@
 #include "bbdg_ept.cuh"
 #include "bbdg_nodal.cuh"
 #include "bbdg_opt.cuh"
+#include "bbdg_tc.cuh"
 
 #ifndef BBDG_T
 #error "BBDG_T (float|double) must be defined"
@@ -106,8 +107,22 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
     nodal_flux_kernel<T, BBDG_N><<<(unsigned)grid, 256, 0, stream>>>(p);
   }
   static DevCache attr;
-  auto kern = nodal_mma_kernel<T, BBDG_N, OP>;
   const int dev = current_device();
+  if constexpr (sizeof(T) == 4) {
+    // fp32: tcgen05 kind::tf32 (3xTF32) with TMEM accumulators (bbdg_tc.cuh)
+    using LT = TcLayout<BBDG_N>;
+    auto kern = nodal_tc_kernel<BBDG_N, OP>;
+    if (attr[dev].load(std::memory_order_acquire) == 0) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, LT::total);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal tc)");
+      attr[dev].store(1, std::memory_order_release);
+    }
+    const int64_t ntiles = (nl + LT::KE - 1) / LT::KE;
+    kern<<<(unsigned)std::min<int64_t>(ntiles, num_sms), LT::threads, LT::total, stream>>>(p);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal tcgen05 kernel launch");
+  }
+  auto kern = nodal_mma_kernel<T, BBDG_N, OP>;
   if (attr[dev].load(std::memory_order_acquire) == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal)");

@@ -117,8 +117,8 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
       if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal tc)");
       attr[dev].store(1, std::memory_order_release);
     }
-    const int64_t ntiles = (nl + LT::KE - 1) / LT::KE;
-    kern<<<(unsigned)std::min<int64_t>(ntiles, num_sms), LT::threads, LT::total, stream>>>(p);
+    const int64_t nsteps = (nl + LT::MT * LT::KE - 1) / (LT::MT * LT::KE);
+    kern<<<(unsigned)std::min<int64_t>(nsteps, num_sms), LT::threads, LT::total, stream>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal tcgen05 kernel launch");
   }

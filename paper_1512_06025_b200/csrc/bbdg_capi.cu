@@ -319,10 +319,77 @@ static int check_aligned(const void* a, const void* b = nullptr, const void* c =
 }
 
 template <typename T>
-static int run(bbdg_ctx* c, int op, int lift, Params<T>& p, void* stream) {
-  KernelEntry k = lookup(c->dtype, c->N, op, lift, c->basis);
+static int run(bbdg_ctx* c, int op, int lift, Params<T>& p, void* stream, int basis = -1) {
+  KernelEntry k = lookup(c->dtype, c->N, op, lift, basis < 0 ? c->basis : basis);
   if (!k.launch) return set_error(BBDG_ERR_UNSUPPORTED, "no kernel for this (op, lift, basis)");
   return k.launch(&p, static_cast<cudaStream_t>(stream), c->num_sms);
+}
+
+// res = a res + dt rhs;  q_out = q_in + b res  (the LSRK stage around a precomputed rhs, solver.py:211-213)
+template <typename T>
+__global__ void stage_update_kernel(int64_t n, const T* __restrict__ q_in, T* __restrict__ q_out, T* __restrict__ res,
+                                    const T* __restrict__ rhs, T a, T b, T dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    T r = res[i] * a;
+    r = r + dt * rhs[i];
+    res[i] = r;
+    q_out[i] = q_in[i] + b * r;
+  }
+}
+
+static int ensure_scratch(void** ptr, size_t bytes, const char* what) {
+  if (*ptr) return BBDG_OK;
+  cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return set_cuda_error(e, what);
+  }
+  return BBDG_OK;
+}
+
+// The Bernstein "dense" lift (bernstein.py:332-347) on the tensor cores: the face fluxes
+// (nodal_flux_kernel) times the dense (Np x 4 Nfp) lift as the lift GEMM of the block-partitioned
+// kernels (tcgen05 kind::tf32 3xTF32 in fp32, DMMA in fp64; the material-scaled epilogue is
+// basis-independent), on top of the Bernstein volume term of the fused kernel.  Whole-mesh calls
+// only (ranges keep the node-per-thread tile kernel).  The flux (and, for the stage, an rhs) scratch
+// is allocated on the first call.
+template <typename T>
+static int bb_dense_tc(bbdg_ctx* c, int op, const void* q, void* out, void* res, double a, double b, double dt,
+                       int accumulate, void* stream) {
+  const size_t sz = sizeof(T);
+  if (int rc = ensure_scratch(&c->flux, (size_t)4 * c->K * 4 * c->Nfp * sz, "dense-lift flux scratch")) return rc;
+  Params<T> p = make_params<T>(c);
+  p.q = static_cast<const T*>(q);
+  T* rhs = static_cast<T*>(op == OP_STAGE ? nullptr : out);
+  if (op == OP_STAGE) {
+    if (int rc = ensure_scratch(&c->rhs_scratch, (size_t)4 * c->K * c->Np * sz, "dense-lift rhs scratch")) return rc;
+    rhs = static_cast<T*>(c->rhs_scratch);
+  }
+  p.out = rhs;
+  if (op != OP_SURFACE) {   // volume term first
+    p.accumulate = 0;
+    if (int rc = run<T>(c, OP_VOLUME, LIFT_OPTIMAL, p, stream)) return rc;
+  }
+  p.flux = static_cast<T*>(c->flux);
+  p.accumulate = op == OP_SURFACE ? accumulate : 1;
+  if (int rc = run<T>(c, OP_SURFACE, LIFT_BLOCKED, p, stream, BBDG_BASIS_NODAL)) return rc;
+  if (op == OP_STAGE) {
+    const int64_t n = (int64_t)4 * c->K * c->Np;
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)c->num_sms * 8);
+    if (n > 0)
+      stage_update_kernel<T><<<(unsigned)grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+          n, static_cast<const T*>(q), static_cast<T*>(out), static_cast<T*>(res), rhs, T(a), T(b), T(dt));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "stage update launch");
+  }
+  return BBDG_OK;
+}
+
+// (measured, cube_mesh(26): the GEMM wins from N = 6 -- fp32 N=9 2.19 vs 2.92 ms, N=7 0.96 vs 1.05; below, the
+// flux round trip through HBM costs more than the node-per-thread kernel's scalar products)
+static bool use_bb_dense_tc(const bbdg_ctx* c, int lift, int64_t k0, int64_t k1) {
+  return c->basis == BBDG_BASIS_BERNSTEIN && lift == LIFT_DENSE && c->N >= 6 && c->blift && c->geo_vol && k0 == 0 &&
+         k1 == c->K && c->nhalo == 0;
 }
 
 extern "C" {
@@ -360,6 +427,7 @@ void bbdg_ctx_destroy(bbdg_ctx* c) {
   cudaFree(c->bvol);
   cudaFree(c->blift);
   cudaFree(c->flux);
+  cudaFree(c->rhs_scratch);
   delete c;
 }
 
@@ -400,10 +468,12 @@ int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* 
     cudaFree(c->liftT);
     c->liftT = c->dtype == BBDG_F32 ? upload(cast<float>(t.data(), t.size()), &rc)
                                     : upload(cast<double>(t.data(), t.size()), &rc);
-    if (c->basis == BBDG_BASIS_NODAL) {
+    {
+      // lift GEMM operator of the tensor-core kernels (nodal blocked path, and the BB "dense" mode)
       const double* m[1] = {dense_L};
       cudaFree(c->blift);
       cudaFree(c->flux);
+      c->flux = nullptr;
       if (c->dtype == BBDG_F32) {   // tcgen05 operator images (bbdg_tc.cuh)
         std::vector<float> vol, lift;
         tc_operator_images(c->N, nullptr, dense_L, vol, lift, tf32_rna);
@@ -411,11 +481,13 @@ int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* 
       } else {
         c->blift = upload(mma_fragments<double>(m, 1, Np, 4 * Nfp), &rc);
       }
-      const size_t fb = (size_t)4 * c->K * 4 * Nfp * (c->dtype == BBDG_F32 ? 4 : 8);
-      cudaError_t e = cudaMalloc(&c->flux, std::max<size_t>(fb, 16));
-      if (e != cudaSuccess) {
-        c->flux = nullptr;
-        rc = set_cuda_error(e, "nodal flux scratch");
+      if (c->basis == BBDG_BASIS_NODAL) {
+        const size_t fb = (size_t)4 * c->K * 4 * Nfp * (c->dtype == BBDG_F32 ? 4 : 8);
+        cudaError_t e = cudaMalloc(&c->flux, std::max<size_t>(fb, 16));
+        if (e != cudaSuccess) {
+          c->flux = nullptr;
+          rc = set_cuda_error(e, "nodal flux scratch");
+        }
       }
     }
   }
@@ -477,6 +549,8 @@ int bbdg_surface(bbdg_ctx* c, const void* q, void* rhs, int lift, int accumulate
   if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q (neighbour traces are read during the call)");
   if (int rc = check_aligned(q, rhs)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
+  if (use_bb_dense_tc(c, lift, 0, c->K))
+    return BBDG_DISPATCH({ return bb_dense_tc<T>(c, OP_SURFACE, q, rhs, nullptr, 0, 0, 0, accumulate, stream); });
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
     p.q = static_cast<const T*>(q);
@@ -498,6 +572,8 @@ int bbdg_rhs_range(bbdg_ctx* c, const void* q, void* rhs, int lift, int64_t k0, 
   if (q == rhs) return set_error(BBDG_ERR_ARG, "rhs must not alias q");
   if (int rc = check_aligned(q, rhs)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
+  if (use_bb_dense_tc(c, lift, k0, k1))
+    return BBDG_DISPATCH({ return bb_dense_tc<T>(c, OP_RHS, q, rhs, nullptr, 0, 0, 0, 0, stream); });
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
     p.q = static_cast<const T*>(q);
@@ -523,6 +599,8 @@ int bbdg_lsrk_stage_range(bbdg_ctx* c, const void* q_in, void* q_out, void* res,
   if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
   if (int rc = check_aligned(q_in, q_out, res)) return rc;
   if (int rc = check_lift(c, lift, true)) return rc;
+  if (use_bb_dense_tc(c, lift, k0, k1))
+    return BBDG_DISPATCH({ return bb_dense_tc<T>(c, OP_STAGE, q_in, q_out, res, rk_a, rk_b, dt, 0, stream); });
   return BBDG_DISPATCH({
     Params<T> p = make_params<T>(c);
     p.q = static_cast<const T*>(q_in);

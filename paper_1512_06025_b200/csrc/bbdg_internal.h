@@ -26,7 +26,8 @@ struct bbdg_ctx {
   void* dT = nullptr;        // T (3,Np,Np)
   void* bvol = nullptr;      // nodal blocked: D_m^T MMA fragments
   void* blift = nullptr;     // nodal blocked: L^T MMA fragments
-  void* flux = nullptr;      // nodal blocked: (4, K, 4 Nfp) face-flux scratch
+  void* flux = nullptr;      // nodal blocked / BB dense on the tensor cores: (4, K, 4 Nfp) face-flux scratch
+  void* rhs_scratch = nullptr;   // BB dense fused stage: (4, K, Np) rhs (allocated on first use)
   const void* halo = nullptr;
   int64_t nhalo = 0;
 };

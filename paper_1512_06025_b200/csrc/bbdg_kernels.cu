@@ -100,7 +100,8 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
   const int64_t nl = p.kend - p.kbeg;
   if (nl == 0) return BBDG_OK;
-  if (!p.bvol || !p.blift || !p.flux) return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded");
+  if ((OP != OP_SURFACE && !p.bvol) || !p.blift || !p.flux)
+    return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded");
   if constexpr (OP != OP_VOLUME) {
     const int64_t n = nl * 4 * Dims<BBDG_N>::Nfp;
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 8);

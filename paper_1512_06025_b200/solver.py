@@ -12,6 +12,7 @@ constructing a ``WaveSystem`` without the library or a CUDA device raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -406,7 +407,7 @@ def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -
     if not torch.from_numpy(q_host).is_pinned():
         # an ordinary (pageable) numpy array: page-lock it for the duration of the step so the chunk
         # copies are asynchronous and overlap the stages (pageable copies serialise with the kernels)
-        if q_host.nbytes < (32 << 20):
+        if q_host.nbytes < (32 << 20) or os.environ.get("BBDG_HOST_REGISTER", "1") == "0":
             return False
         if int(torch._C._cudart.cudaHostRegister(q_host.ctypes.data, q_host.nbytes, 0)) != 0:
             return False   # registration refused: the plain copy path

@@ -407,7 +407,9 @@ def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -
     if not torch.from_numpy(q_host).is_pinned():
         # an ordinary (pageable) numpy array: page-lock it for the duration of the step so the chunk
         # copies are asynchronous and overlap the stages (pageable copies serialise with the kernels)
-        if q_host.nbytes < (32 << 20) or os.environ.get("BBDG_HOST_REGISTER", "1") == "0":
+        # (measured on the B200 boxes: page-locking costs ~5 GB/s, a win for states up to several hundred
+        # MB -- cube_mesh(40) N=5, 344 MB: 50 -> 26 ms per step -- and a loss above ~1 GB: N=9 194 -> 294 ms)
+        if not (32 << 20) <= q_host.nbytes <= (768 << 20) or os.environ.get("BBDG_HOST_REGISTER", "1") == "0":
             return False
         if int(torch._C._cudart.cudaHostRegister(q_host.ctypes.data, q_host.nbytes, 0)) != 0:
             return False   # registration refused: the plain copy path

@@ -431,6 +431,7 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=16, help="oracle sample mesh cube_mesh(cpu_n)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodal", dest="nodal", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-state end-to-end leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
@@ -485,18 +486,18 @@ def main():
                                "per_order": r["per_order"]} for d, r in per_dtype.items()})
     if world > 1:
         line["nccl"] = {"backend": "nccl", "nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version()))}
-    if world == 1 and not args.quick:
+    if world == 1 and not args.quick and args.e2e:
         e2e = e2e_host(args, head)
         line["e2e"] = {"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["bytes_per_step"],
                        "d2h_bytes_per_step": e2e["bytes_per_step"], "pageable_value": e2e["pageable_value"],
                        "what": f"lsrk4_step (5 fused stages) on a host numpy state per order, {e2e['mesh']}: H2D + "
                                "stages + D2H in the timed region (pinned: chunk-pipelined bbdg_step_host; "
                                "pageable_value: an ordinary numpy array)", "per_order": e2e["per_order"]}
-        if args.nodal:
-            line["comparison"] = compare_bases(args, head)
     else:
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                       "what": "not measured in --quick / multi-GPU mode"}
+                       "what": "not measured in --quick / --no-e2e / multi-GPU mode"}
+    if world == 1 and not args.quick and args.nodal:
+        line["comparison"] = compare_bases(args, head)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dtype = np.float32 if head == "f32" else np.float64
         reps, K, procs = cpu_sweep(orders, args.cpu_n, dtype, lifts=(args.lift, "factorized"), reps=2)

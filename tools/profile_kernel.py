@@ -22,15 +22,23 @@ def main():
     ap.add_argument("--basis", default="bernstein")
     ap.add_argument("--n", type=int, default=26)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--box", default=None, help="nx,ny,nz: a device-built BoxMesh (e.g. the bench's fill mesh)")
     a = ap.parse_args()
     import torch
 
     from paper_1512_06025_b200 import BernsteinRefOps, Materials, NodalRefOps, WaveSystem, cube_mesh
     from paper_1512_06025_b200.solver import RK4A, RK4B, _device_update
 
-    m = cube_mesh(a.n)
     ops = BernsteinRefOps.build(a.N) if a.basis == "bernstein" else NodalRefOps.build(a.N)
-    sy = WaveSystem(m, ops, Materials.homogeneous(m.K), dtype=np.float32 if a.dtype == "f32" else np.float64)
+    dt = np.float32 if a.dtype == "f32" else np.float64
+    if a.box:
+        from paper_1512_06025_b200.mesh_device import BoxMesh
+
+        m = BoxMesh(*[int(x) for x in a.box.split(",")])
+        sy = WaveSystem(m, ops, Materials(np.float64(1.0), np.float64(1.0)), dtype=dt, legacy_records=False)
+    else:
+        m = cube_mesh(a.n)
+        sy = WaveSystem(m, ops, Materials.homogeneous(m.K), dtype=dt)
     g = torch.Generator(device="cuda").manual_seed(1)
     q = torch.randn((4, m.K, sy.Np), dtype=sy.torch_dtype, device="cuda", generator=g)
     q2, res, rhs = torch.empty_like(q), torch.randn_like(q), torch.empty_like(q)

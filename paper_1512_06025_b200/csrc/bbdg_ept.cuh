@@ -77,9 +77,8 @@ template <typename T, int N> struct EptLayout {
   static constexpr int rnd(int n) { return (n + A - 1) / A * A; }
   static constexpr int FQ = rnd(KE * Np);                 // field plane stride in the stage
   static constexpr int s_q = 0, s_res = 4 * FQ, s_geo = 8 * FQ, stage_T = rnd(s_geo + KE * kGeoRec);
-  static constexpr int nb_T = rnd(4 * KE * ES);           // trace buffer (also holds the tile's rhs)
-  static_assert(nb_T >= 4 * FQ, "rhs aliases a trace buffer");
-  static constexpr int w_stage0 = 0, w_nb0 = 2 * stage_T, w_conn = w_nb0 + 2 * nb_T;   // units of T
+  static constexpr int nb_T = rnd(4 * KE * ES);           // trace buffer (one: refilled mid-tile)
+  static constexpr int w_stage0 = 0, w_nb0 = 2 * stage_T, w_conn = w_nb0 + nb_T;   // units of T
   static constexpr int w_bar = rnd(w_conn + (KE * 5 * 4 + sz - 1) / sz);                 // 2 mbarriers
   static constexpr int warp_bytes = (w_bar + 16 / sz) * sz;
   static constexpr int o_tr2 = 0;                                   // u16 [4 f2][6 perm][Nfp]
@@ -124,20 +123,19 @@ __device__ __forceinline__ void pair_sync(int pair) {
 //   role 0: dp = -kappa div u + kappa L(Fp)       (u1, u2, u3 in registers; own p traces from smem)
 //   role 1: du_i = -(1/rho) dp/dx_i + (1/rho) L(n_i Fu)   (p in registers; own u traces from smem)
 // Both evaluate the upwind flux at every face point (Fp needs the u jump, Fu the p jump).
+template <int ROLE> struct EptRole {
+  static constexpr int NF = ROLE == 0 ? 3 : 1;   // fields held in registers
+  static constexpr int F0 = ROLE == 0 ? 1 : 0;   // first of them
+  static constexpr int NR = ROLE == 0 ? 1 : 3;   // rhs fields produced
+};
+
+// volume term (solver.py:139-158) added to r
 template <int ROLE, typename T, int N, class L>
-__device__ __forceinline__ void ept_compute(const T* __restrict__ sq, const T* __restrict__ gr,
-                                            const T* __restrict__ snb, int lane, T (&r)[ROLE == 0 ? 1 : 3][L::Np]) {
-  constexpr int Np = L::Np, Nfp = L::Nfp, Npm = L::Npm, KE = L::KE, ES = L::ES, NFS = L::NFS;
-  constexpr int NF = ROLE == 0 ? 3 : 1;      // fields held in registers
-  constexpr int F0 = ROLE == 0 ? 1 : 0;      // first of them
-  constexpr int NR = ROLE == 0 ? 1 : 3;      // rhs fields produced
-  T qv[NF][Np];
-#pragma unroll
-  for (int F = 0; F < NF; ++F)
-#pragma unroll
-    for (int i = 0; i < Np; i += L::QV) ld_vec<T, L::QV>(sq + (F0 + F) * L::FQ + lane * Np + i, &qv[F][i]);
+__device__ __forceinline__ void ept_volume(const T* __restrict__ gr, const T (&qv)[EptRole<ROLE>::NF][L::Np],
+                                           T (&r)[EptRole<ROLE>::NR][L::Np]) {
+  constexpr int Np = L::Np, Npm = L::Npm;
+  constexpr int NF = EptRole<ROLE>::NF, NR = EptRole<ROLE>::NR;
   const T kap = gr[24], irho = gr[25];
-  // ---------------------------------------------------------------- volume (solver.py:139-158)
   {
     T G[9];
 #pragma unroll
@@ -180,11 +178,20 @@ __device__ __forceinline__ void ept_compute(const T* __restrict__ sq, const T* _
             acc += T(al.a[j]) * w[F][bj];
           }
         });
-        r[F][decltype(I)::value] = acc;
+        r[F][decltype(I)::value] += acc;
       }
     });
   }
-  // ---------------------------------------------------------------- surface (solver.py:166-190)
+}
+
+// surface term (solver.py:166-190) added to r
+template <int ROLE, typename T, int N, class L>
+__device__ __forceinline__ void ept_surface(const T* __restrict__ sq, const T* __restrict__ gr,
+                                            const T* __restrict__ snb, int lane,
+                                            const T (&qv)[EptRole<ROLE>::NF][L::Np], T (&r)[EptRole<ROLE>::NR][L::Np]) {
+  constexpr int Np = L::Np, Nfp = L::Nfp, KE = L::KE, ES = L::ES, NFS = L::NFS;
+  constexpr int NR = EptRole<ROLE>::NR;
+  const T kap = gr[24], irho = gr[25];
   static_for<0, 4>([&](auto FF) {
     constexpr int f = decltype(FF)::value;
     const V4<T> nf = *reinterpret_cast<const V4<T>*>(gr + 4 * f);
@@ -266,6 +273,18 @@ __device__ __forceinline__ void ept_compute(const T* __restrict__ sq, const T* _
       });
     });
   });
+}
+
+template <typename T, int W> __device__ __forceinline__ void st_global_vec(T* g, const T* r) {
+  if constexpr (W == 4) {
+    __stcs(reinterpret_cast<float4*>(g), make_float4(r[0], r[1], r[2], r[3]));
+  } else if constexpr (W == 2 && sizeof(T) == 4) {
+    __stcs(reinterpret_cast<float2*>(g), make_float2(r[0], r[1]));
+  } else if constexpr (W == 2) {
+    __stcs(reinterpret_cast<double2*>(g), make_double2(r[0], r[1]));
+  } else {
+    __stcs(g, r[0]);
+  }
 }
 
 template <typename T, int N, int OP>
@@ -404,103 +423,87 @@ __global__ void __launch_bounds__(EptLayout<T, N>::threads, 1) ept_kernel(const 
       if (tn < ntiles) load_conn(tile_k0(tn), tile_nv(tn));
     }
   }
+  using R0 = EptRole<0>;
+  using R1 = EptRole<1>;
   for (int it = 0; tile < ntiles; tile += stride, ++it) {
     const int st = it & 1;
     const int64_t k0 = tile_k0(tile);
     const int nv = tile_nv(tile);
     const int64_t tn = tile + stride, tn2 = tn + stride;
-    if (role == 1) {
-      if (tn < ntiles) {
-        fence_proxy_async();
-        issue_state(tile_k0(tn), tile_nv(tn), st ^ 1);
-      }
-    } else {
-      if (tn < ntiles) {
-        issue_nb(tile_k0(tn), tile_nv(tn), st ^ 1);
-        if (tn2 < ntiles) load_conn(tile_k0(tn2), tile_nv(tn2));
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this tile's traces landed
-      } else {
-        cp_async_wait_all();
-      }
+    if (role == 1 && tn < ntiles) {
+      fence_proxy_async();
+      issue_state(tile_k0(tn), tile_nv(tn), st ^ 1);
     }
+    if (role == 0) cp_async_wait_all();   // this tile's traces landed
     mbar_wait(bars + st, (it >> 1) & 1);
     pair_sync(pair);   // the state (TMA) and the traces (role 0's cp.async) are visible to both warps
 
     const T* sq = stage_ptr(st) + L::s_q;
     const T* sres = stage_ptr(st) + L::s_res;
     const T* gr = stage_ptr(st) + L::s_geo + lane * kGeoRec;
-    T* snb = nb_ptr(st);
-    T* srhs = snb;   // the tile's rhs, once both warps are done with the traces
-    if (role == 0) {
-      T r[1][Np];
-      ept_compute<0, T, N, L>(sq, gr, snb, lane, r);
+    const T* snb = nb_ptr(0);
+    // surface first: the trace buffer is then free for the next tile's gather, which overlaps the
+    // volume term and the epilogue of this one
+    auto finish = [&](auto role_c, auto& qv, auto& r) {
+      constexpr int RL = decltype(role_c)::value;
+      using RR = EptRole<RL>;
+      ept_surface<RL, T, N, L>(sq, gr, snb, lane, qv, r);
       pair_sync(pair);
+      if (RL == 0 && tn < ntiles) {
+        issue_nb(tile_k0(tn), tile_nv(tn), 0);
+        if (tn2 < ntiles) load_conn(tile_k0(tn2), tile_nv(tn2));
+      }
+      ept_volume<RL, T, N, L>(gr, qv, r);
+      // epilogue per lane (element), 8/16-byte streaming stores straight from registers
+      if (lane < nv) {
 #pragma unroll
-      for (int i = 0; i < Np; i += L::QV) st_vec<T, L::QV>(srhs + lane * Np + i, &r[0][i]);
-    } else {
-      T r[3][Np];
-      ept_compute<1, T, N, L>(sq, gr, snb, lane, r);
-      pair_sync(pair);
+        for (int F = 0; F < RR::NR; ++F) {
+          const int Fg = RL == 0 ? 0 : 1 + F;
+          const int64_t o = Fg * fs + (k0 + lane) * Np;
 #pragma unroll
-      for (int F = 0; F < 3; ++F)
-#pragma unroll
-        for (int i = 0; i < Np; i += L::QV) st_vec<T, L::QV>(srhs + (1 + F) * L::FQ + lane * Np + i, &r[F][i]);
-    }
-    pair_sync(pair);
-    // ------------------------------------------------------------ epilogue over contiguous words (both warps)
-    const int nw = nv * Np, t64 = role * 32 + lane;
-#pragma unroll
-    for (int F = 0; F < 4; ++F) {
-      T* outF = p.out + F * fs + k0 * Np;
-      T* resF = p.res + F * fs + k0 * Np;
-      const T* qF = sq + F * L::FQ;
-      const T* rF = srhs + F * L::FQ;
-      const T* sF = sres + F * L::FQ;
-      for (int w0 = t64 * A; w0 < nw; w0 += 64 * A) {
-        if (w0 + A <= nw) {
-          T x[A], o[A], rr[A], qq[A], ss[A];
-          ld_vec<T, A>(rF + w0, rr);
-          if constexpr (STAGE) {
-            ld_vec<T, A>(qF + w0, qq);
-            ld_vec<T, A>(sF + w0, ss);
-#pragma unroll
-            for (int u = 0; u < A; ++u) {
-              x[u] = ss[u] * p.rk_a;
-              x[u] = x[u] + p.dt * rr[u];
-              o[u] = qq[u] + p.rk_b * x[u];
-            }
-            if constexpr (A == 4) {
-              __stcs(reinterpret_cast<float4*>(resF + w0), make_float4(x[0], x[1], x[2], x[3]));
-              __stcs(reinterpret_cast<float4*>(outF + w0), make_float4(o[0], o[1], o[2], o[3]));
-            } else {
-              __stcs(reinterpret_cast<double2*>(resF + w0), make_double2(x[0], x[1]));
-              __stcs(reinterpret_cast<double2*>(outF + w0), make_double2(o[0], o[1]));
-            }
-          } else {
-            if (p.accumulate) {
-#pragma unroll
-              for (int u = 0; u < A; ++u) outF[w0 + u] += rr[u];
-            } else {
-#pragma unroll
-              for (int u = 0; u < A; ++u) st_stream(outF + w0 + u, rr[u]);
-            }
-          }
-        } else {
-          for (int w = w0; w < nw; ++w) {
+          for (int i = 0; i < Np; i += L::QV) {
+            T x[L::QV], y[L::QV];
             if constexpr (STAGE) {
-              T x = sF[w] * p.rk_a;
-              x = x + p.dt * rF[w];
-              st_stream(resF + w, x);
-              st_stream(outF + w, qF[w] + p.rk_b * x);
+              T ss[L::QV], qq[L::QV];
+              ld_vec<T, L::QV>(sres + Fg * L::FQ + lane * Np + i, ss);
+              ld_vec<T, L::QV>(sq + Fg * L::FQ + lane * Np + i, qq);
+#pragma unroll
+              for (int u = 0; u < L::QV; ++u) {
+                x[u] = ss[u] * p.rk_a;
+                x[u] = x[u] + p.dt * r[F][i + u];
+                y[u] = qq[u] + p.rk_b * x[u];
+              }
+              st_global_vec<T, L::QV>(p.res + o + i, x);
+              st_global_vec<T, L::QV>(p.out + o + i, y);
             } else {
-              if (p.accumulate) outF[w] += rF[w];
-              else st_stream(outF + w, rF[w]);
+#pragma unroll
+              for (int u = 0; u < L::QV; ++u) y[u] = p.accumulate ? p.out[o + i + u] + r[F][i + u] : r[F][i + u];
+              st_global_vec<T, L::QV>(p.out + o + i, y);
             }
           }
         }
       }
+    };
+    if (role == 0) {
+      T qv[R0::NF][Np], r[R0::NR][Np];
+#pragma unroll
+      for (int F = 0; F < R0::NF; ++F)
+#pragma unroll
+        for (int i = 0; i < Np; i += L::QV) ld_vec<T, L::QV>(sq + (R0::F0 + F) * L::FQ + lane * Np + i, &qv[F][i]);
+#pragma unroll
+      for (int i = 0; i < Np; ++i) r[0][i] = T(0);
+      finish(std::integral_constant<int, 0>{}, qv, r);
+    } else {
+      T qv[R1::NF][Np], r[R1::NR][Np];
+#pragma unroll
+      for (int i = 0; i < Np; i += L::QV) ld_vec<T, L::QV>(sq + lane * Np + i, &qv[0][i]);
+#pragma unroll
+      for (int F = 0; F < R1::NR; ++F)
+#pragma unroll
+        for (int i = 0; i < Np; ++i) r[F][i] = T(0);
+      finish(std::integral_constant<int, 1>{}, qv, r);
     }
-    pair_sync(pair);   // this stage / trace buffer is free for the tile after next
+    pair_sync(pair);   // this stage buffer is free for the tile after next
   }
 }
 

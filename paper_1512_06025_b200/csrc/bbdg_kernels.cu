@@ -65,7 +65,7 @@ template <int OP, int FSR> int launch_opt(const void* vp, cudaStream_t stream, i
 }
 
 #ifndef BBDG_EPT_MAX_N
-#define BBDG_EPT_MAX_N 2   // element-per-thread register kernels for N <= this (bbdg_ept.cuh)
+#define BBDG_EPT_MAX_N 3   // element-per-thread register kernels for N <= this (bbdg_ept.cuh)
 #endif
 #ifndef BBDG_EPT_MAX_N64
 #define BBDG_EPT_MAX_N64 2

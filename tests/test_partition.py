@@ -198,7 +198,8 @@ class _FakeDist:
 @pytest.mark.gpu
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("dname", ["f64", "f32"])
-def test_partitioned_step_bitwise_equals_single_domain(P, dname):
+@pytest.mark.parametrize("N", [4, 9])
+def test_partitioned_step_bitwise_equals_single_domain(P, dname, N):
     import torch
 
     from paper_1512_06025_b200 import Materials, WaveSystem, stable_dt
@@ -207,7 +208,6 @@ def test_partitioned_step_bitwise_equals_single_domain(P, dname):
 
     dtype = np.float64 if dname == "f64" else np.float32
     m = msh.cube_mesh(6)
-    N = 4
     ops = BernsteinRefOps.build(N)
     mat = Materials.homogeneous(m.K)
     single = WaveSystem(m, ops, mat, dtype)

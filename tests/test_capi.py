@@ -72,3 +72,26 @@ def test_python_layer_fails_loudly_without_gpu():
     m = cube_mesh(1)
     with pytest.raises(_lib.BBDGError):
         WaveSystem(m, BernsteinRefOps.build(2), Materials.homogeneous(m.K))
+
+
+def test_round2_entry_points_validate_without_compute():
+    """Argument checks of the round-2 entry points return before any device work."""
+    lib = _lib.load()
+    ctx = C.c_void_p()
+    assert lib.bbdg_ctx_create(3, 0, 0, 6 * 2 * 3 * 4, C.byref(ctx)) == 0
+    lo, hi = (C.c_double * 3)(0, 0, 0), (C.c_double * 3)(1, 1, 1)
+    try:
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 0, 3, 4, 0, 0, lo, hi, 1.0, 1.0, 0, None) == 1      # nx < 1
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 1, 1, lo, hi, 1.0, 1.0, 0, None) == 1      # empty slab
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 3, 3, 4, 0, 3, lo, hi, 1.0, 1.0, 0, None) == 1      # K mismatch
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, lo, hi, -1.0, 1.0, 0, None) == 1     # kappa <= 0
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, hi, lo, 1.0, 1.0, 0, None) == 1      # hi <= lo
+        assert b"hi > lo" in lib.bbdg_last_error()
+        assert lib.bbdg_step2(ctx, 16, 32, 16, 48, 0.1, 1, None) == 2                             # no geometry
+    finally:
+        lib.bbdg_ctx_destroy(ctx)
+    assert lib.bbdg_ops_grad(0, 0, 4, 16, 16, 16, 16, None) == 2       # degree outside 1..20
+    assert lib.bbdg_ops_lift(21, 0, 4, 16, 16, None) == 2
+    assert lib.bbdg_ops_grad(3, 0, 0, None, None, None, None, None) == 0   # empty batch: nothing to do
+    assert lib.bbdg_dense_apply(0, 4, 0, 3, 16, 16, 16, None) == 1     # nrows < 1
+    assert lib.bbdg_dense_apply(5, 4, 2, 3, 16, 16, 16, None) == 1     # dtype

@@ -41,7 +41,8 @@ def main():
         sy = WaveSystem(m, ops, Materials.homogeneous(m.K), dtype=dt)
     g = torch.Generator(device="cuda").manual_seed(1)
     q = torch.randn((4, m.K, sy.Np), dtype=sy.torch_dtype, device="cuda", generator=g)
-    q2, res, rhs = torch.empty_like(q), torch.randn_like(q), torch.empty_like(q)
+    q2, res = torch.empty_like(q), torch.randn_like(q)
+    rhs = torch.empty_like(q) if a.op in ("volume", "surface", "rhs", "update") else None
     for _ in range(a.reps):
         if a.op == "stage":
             sy.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, a.lift)

@@ -26,8 +26,8 @@ def main(path, box_k_json=None):
     fam = defaultdict(list)
     for lid, m in per.items():
         name = m["name"]
-        mo = re.match(r"void bbdg::(opt_kernel|ept_kernel)<(float|double), (\d), (\d)", name)
-        mu = re.match(r"void bbdg::lsrk_update_vec_kernel<(float|double)", name)
+        mo = re.match(r"void (?:bbdg::)?(opt_kernel|ept_kernel)<(float|double), (\d), (\d)", name)
+        mu = re.match(r"void (?:bbdg::)?lsrk_update_vec_kernel<(float|double)", name)
         if mo:
             key = (mo.group(2), int(mo.group(3)), OPS[mo.group(4)])
         elif mu:

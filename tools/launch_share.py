@@ -7,7 +7,7 @@ from collections import defaultdict
 
 
 def family(name):
-    m = re.match(r"void bbdg::(\w+)<([^>]*)>", name)
+    m = re.match(r"void (?:bbdg::)?(\w+)<([^>]*)>", name)
     if m:
         return f"bbdg::{m.group(1)}<{m.group(2)}>"
     return "torch/other: " + name.split("(")[0][:60]

@@ -143,7 +143,12 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------- GPU arm
-def fill_box(N, s, budget_bytes, ranks=1):
+# element order of the HBM-filling boxes: slabs of 4 x-layers, (y, z, x) inside a slab, so every neighbour
+# except those across a slab face lies within a few MB (L2) of its element (bbdg_ctx_set_box_mesh)
+XBLOCK = 4
+
+
+def fill_box(N, s, budget_bytes, ranks=1, xblock=1):
     """A Kuhn box (nx, n, n) whose resident bytes fit budget_bytes (per rank: nx a multiple of
     `ranks` layers per rank), as cubic as possible."""
     from paper_1512_06025_b200.mesh_device import BoxMesh
@@ -151,8 +156,8 @@ def fill_box(N, s, budget_bytes, ranks=1):
     per = resident_bytes(N, s, 1)
     k_max = min(int(budget_bytes // per), (1 << 29) - 1)     # int32 face ids: 4 K < 2^31
     n = max(1, int((k_max / 6) ** (1.0 / 3.0)))
-    nx = max(1, k_max // (6 * n * n))
-    return BoxMesh(nx * ranks, n, n, lo=(-0.5 * ranks, -0.5, -0.5), hi=(0.5 * ranks, 0.5, 0.5))
+    nx = max(xblock, k_max // (6 * n * n) // xblock * xblock)
+    return BoxMesh(nx * ranks, n, n, lo=(-0.5 * ranks, -0.5, -0.5), hi=(0.5 * ranks, 0.5, 0.5), xblock=xblock)
 
 
 def events_time(torch, fn, reps, sync_group=None):
@@ -196,7 +201,7 @@ def run_dtype(args, dname, rank, world, dev, peak, clocks):
         torch.cuda.empty_cache()
         budget = args.fill * (total_mem - torch.cuda.memory_allocated(dev))
         if world == 1:
-            box = fill_box(N, s, budget)
+            box = fill_box(N, s, budget, 1, XBLOCK)
             sy = WaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
                             legacy_records=False)
             K = box.K
@@ -204,10 +209,10 @@ def run_dtype(args, dname, rank, world, dev, peak, clocks):
             if args.strong:   # the 1-GPU mesh, split over the ranks (needs nx >= world layers)
                 from paper_1512_06025_b200.mesh_device import BoxMesh
 
-                one = fill_box(N, s, budget)
-                box = BoxMesh(max(one.nx, world), one.ny, one.nz)
+                one = fill_box(N, s, budget, 1, XBLOCK)
+                box = BoxMesh(max(one.nx, world * XBLOCK), one.ny, one.nz, xblock=XBLOCK)
             else:             # weak: an HBM-filling slab per rank
-                box = fill_box(N, s, budget, world)
+                box = fill_box(N, s, budget, world, XBLOCK)
             sy = DistWaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
                                 rank, world, legacy_records=False)
             K = sy.K
@@ -441,7 +446,8 @@ def main():
     head = dnames[0]
     scaling = "strong" if (args.strong and world > 1) else "weak"
     config = {"workload": WORKLOAD.format(orders=args.orders, lift=args.lift), "orders": orders, "lift": args.lift,
-              "mesh": f"per order a device-built Kuhn box filling {args.fill:.2f} of free HBM"
+              "mesh": f"per order a device-built Kuhn box filling {args.fill:.2f} of free HBM, element order in "
+                      f"slabs of {XBLOCK} x-layers"
                       + (f" per rank (x-layer slabs, {scaling} scaling)" if world > 1 else ""),
               "l2": "not flushed: every launch streams >= 1.4 GB (inputs larger than the 126 MB L2)",
               "materials": "homogeneous (kappa = rho = 1)",

@@ -69,11 +69,13 @@ int bbdg_ctx_set_geometry(bbdg_ctx* ctx, const double* rst_dx, const double* kap
  * index arithmetic -- no host arrays (HBM-filling meshes; slab-local setup of partitioned runs).
  * The context holds the cell layers [cx0, cx1) (K = 6 (cx1 - cx0) ny nz, x-slab-major element
  * order); faces into layers outside the slab but inside the box are halo faces whose slots follow
- * partition.build_halo_plan's order.  Homogeneous materials kappa, rho.  legacy_records = 0 builds
+ * partition.build_halo_plan's order.  xblock = 1 is that (reference) order; xblock > 1 orders the
+ * cells in slabs of xblock x-layers, (y, z, x) inside a slab, so x-neighbours sit 6 elements apart
+ * (cx0 and cx1 multiples of xblock).  Homogeneous materials kappa, rho.  legacy_records = 0 builds
  * only the fused record of the hot-path kernels (the ELL, dense and nodal kernels then return
  * BBDG_ERR_UNSUPPORTED).  Synchronises `stream` (setup call). */
-int bbdg_ctx_set_box_mesh(bbdg_ctx* ctx, int nx, int ny, int nz, int cx0, int cx1, const double* lo, const double* hi,
-                          double kappa, double rho, int legacy_records, void* stream);
+int bbdg_ctx_set_box_mesh(bbdg_ctx* ctx, int nx, int ny, int nz, int cx0, int cx1, int xblock, const double* lo,
+                          const double* hi, double kappa, double rho, int legacy_records, void* stream);
 
 /* Lift tables (host, float64): E_L as ELL (Np, width) for the "factorized"
  * mode (bernstein.py:273-310) and the dense (Np, 4 Nfp) lift for "dense"

@@ -31,8 +31,8 @@ SIGNATURES = [
     ("bbdg_ctx_create", C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.POINTER(_P)]),
     ("bbdg_ctx_destroy", None, [_P]),
     ("bbdg_ctx_set_geometry", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    ("bbdg_ctx_set_box_mesh", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _D, _D, C.c_int,
-                                        _P]),
+    ("bbdg_ctx_set_box_mesh", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, _D, _D,
+                                        C.c_int, _P]),
     ("bbdg_ctx_set_lift_tables", C.c_int, [_P, _P, _P, C.c_int, _P]),
     ("bbdg_ctx_set_nodal_ops", C.c_int, [_P, _P, _P, _P]),
     ("bbdg_ctx_set_halo", C.c_int, [_P, _P, _I64]),

@@ -4,8 +4,8 @@
 // element, with no host arrays and no transient device memory -- so meshes that fill a B200's
 // HBM set up in milliseconds, and each rank of a slab partition builds only its own slab.
 //
-// Element e of the slab [cx0, cx1) x ny x nz cells is tet t = e mod 6 of cell
-// (ci, cj, ck) = x-slab-major cell cx0 ny nz + e / 6: the lattice path c, c + e_p0,
+// Element e of the slab [cx0, cx1) x ny x nz cells is tet t = e mod 6 of cell e / 6 in the
+// (x-blocked, see cell_lin) cell order counted from layer cx0: the lattice path c, c + e_p0,
 // c + e_p0 + e_p1, c + (1,1,1) for the axis permutation p = AXIS_PERMS[t] (mesh.box_mesh),
 // with vertices 1 and 2 swapped for odd permutations (mesh._orient).  Face f is opposite
 // vertex f (multiindex.FACE_VERTICES).  The neighbour across the face opposite path vertex
@@ -31,6 +31,7 @@ __device__ const int kPerms3[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}
 struct Box {
   int nx, ny, nz;        // global cells
   int cx0, cx1;          // this slab's cell layers
+  int xb;                // x-blocking of the element order (1 = the reference's x-slab-major order)
   double lo[3], step[3], hi[3];
   double kappa, inv_rho, tau_p, tau_u;
 };
@@ -59,6 +60,27 @@ __device__ void tet_vertices(const int c[3], int t, int v[4][3]) {
 
 __device__ __forceinline__ bool same(const int* a, const int* b) { return a[0] == b[0] && a[1] == b[1] && a[2] == b[2]; }
 
+// Cell order: slabs of xb x-layers (the last one may be thinner), slab-major; inside a slab the cells
+// run (y, z, x) with x fastest.  xb = 1 is the reference's x-slab-major cube_mesh order; xb > 1 puts
+// the x-neighbours of a cell 6 elements apart (the y-neighbours 6 xb nz apart), so an HBM-filling
+// mesh reads its neighbour traces from L2 instead of DRAM (only the faces between slabs are far).
+__device__ __forceinline__ int64_t cell_lin(const Box& b, int cx, int cy, int cz) {
+  const int s = cx / b.xb, ts = min(b.xb, b.nx - s * b.xb);
+  return (int64_t)s * b.xb * b.ny * b.nz + ((int64_t)cy * b.nz + cz) * ts + (cx - s * b.xb);
+}
+__device__ __forceinline__ void cell_of(const Box& b, int64_t lin, int c[3]) {
+  const int64_t slab = (int64_t)b.xb * b.ny * b.nz;
+  const int nslab = (b.nx + b.xb - 1) / b.xb;
+  int64_t s = lin / slab;
+  if (s > nslab - 1) s = nslab - 1;
+  const int64_t rem = lin - s * slab;
+  const int ts = min(b.xb, b.nx - (int)s * b.xb);
+  const int64_t yz = rem / ts;
+  c[0] = (int)(s * b.xb + (rem - yz * ts));
+  c[1] = (int)(yz / b.nz);
+  c[2] = (int)(yz - (int64_t)c[1] * b.nz);
+}
+
 // numpy.linspace(lo, hi, n + 1)[i] = i * step + lo (last point = hi), no FMA contraction
 __device__ __forceinline__ double coord(const Box& b, int axis, int i) {
   const int n = axis == 0 ? b.nx : (axis == 1 ? b.ny : b.nz);
@@ -71,9 +93,10 @@ __global__ void box_mesh_kernel(Box b, int64_t K, T* __restrict__ geo, T* __rest
   const int64_t plane = (int64_t)b.ny * b.nz;
   const int nleft = b.cx0 > 0 ? 2 * b.ny * b.nz : 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cell = (int64_t)b.cx0 * plane + e / 6;
+    const int64_t base = (int64_t)b.cx0 * plane;   // cx0 is a multiple of xb: full slabs before it
     const int t = (int)(e % 6);
-    const int c[3] = {(int)(cell / plane), (int)((cell % plane) / b.nz), (int)(cell % b.nz)};
+    int c[3];
+    cell_of(b, base + e / 6, c);
     int v[4][3];
     tet_vertices(c, t, v);
     double x[4][3];
@@ -163,7 +186,7 @@ __global__ void box_mesh_kernel(Box b, int64_t K, T* __restrict__ geo, T* __rest
         nb[f] = nleft + 2 * (c[1] * b.nz + c[2]) + t;
         code[f] |= 1 << 6;
       } else {
-        nb[f] = (int32_t)(((int64_t)(c2[0] - b.cx0) * plane + (int64_t)c2[1] * b.nz + c2[2]) * 6 + t2);
+        nb[f] = (int32_t)((cell_lin(b, c2[0], c2[1], c2[2]) - base) * 6 + t2);
       }
     }
     pack_element<T>(rst_dx, b.kappa, b.inv_rho, normals, fscale, taup, tauu, nb, code, geo + e * kGeoRec,
@@ -208,16 +231,19 @@ template <typename T> int build_box(bbdg_ctx* c, const Box& b, bool legacy, cuda
 
 using namespace bbdg;
 
-extern "C" int bbdg_ctx_set_box_mesh(bbdg_ctx* c, int nx, int ny, int nz, int cx0, int cx1, const double* lo,
-                                     const double* hi, double kappa, double rho, int legacy_records, void* stream) {
+extern "C" int bbdg_ctx_set_box_mesh(bbdg_ctx* c, int nx, int ny, int nz, int cx0, int cx1, int xblock,
+                                     const double* lo, const double* hi, double kappa, double rho, int legacy_records,
+                                     void* stream) {
   if (!c || !lo || !hi) return set_error(BBDG_ERR_ARG, "null argument");
   if (nx < 1 || ny < 1 || nz < 1 || cx0 < 0 || cx1 > nx || cx0 >= cx1)
     return set_error(BBDG_ERR_ARG, "bad box dimensions or slab");
+  if (xblock < 1 || cx0 % xblock != 0 || (cx1 % xblock != 0 && cx1 != nx))
+    return set_error(BBDG_ERR_ARG, "slab layers must be multiples of the x-blocking");
   if (c->K != 6LL * (cx1 - cx0) * ny * nz) return set_error(BBDG_ERR_ARG, "context K != 6 (cx1 - cx0) ny nz");
   if (!(kappa > 0.0) || !(rho > 0.0)) return set_error(BBDG_ERR_ARG, "kappa and rho must be positive");
   if (4LL * c->K >= (1LL << 31) || 4LL * ny * nz >= (1LL << 31)) return set_error(BBDG_ERR_ARG, "box too large for int32 ids");
   Box b{};
-  b.nx = nx, b.ny = ny, b.nz = nz, b.cx0 = cx0, b.cx1 = cx1;
+  b.nx = nx, b.ny = ny, b.nz = nz, b.cx0 = cx0, b.cx1 = cx1, b.xb = xblock;
   const int n[3] = {nx, ny, nz};
   for (int i = 0; i < 3; ++i) {
     if (!(hi[i] > lo[i])) return set_error(BBDG_ERR_ARG, "box must have hi > lo");

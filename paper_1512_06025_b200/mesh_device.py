@@ -123,16 +123,19 @@ class BoxMesh:
     """
 
     def __init__(self, nx: int, ny: int, nz: int, lo=(-0.5, -0.5, -0.5), hi=(0.5, 0.5, 0.5), cx0: int = 0,
-                 cx1: int | None = None):
-        if min(nx, ny, nz) < 1:
+                 cx1: int | None = None, xblock: int = 1):
+        if min(nx, ny, nz) < 1 or xblock < 1:
             raise ValueError("need at least one cell per axis")
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.xblock = int(xblock)   # element order: slabs of xblock x-layers (1 = reference cube_mesh order)
         self.lo = tuple(float(x) for x in lo)
         self.hi = tuple(float(x) for x in hi)
         self.cx0 = int(cx0)
         self.cx1 = self.nx if cx1 is None else int(cx1)
         if not 0 <= self.cx0 < self.cx1 <= self.nx:
             raise ValueError("slab layers must satisfy 0 <= cx0 < cx1 <= nx")
+        if self.cx0 % self.xblock or (self.cx1 % self.xblock and self.cx1 != self.nx):
+            raise ValueError("slab layers must be multiples of the x-blocking")
         # every cell is the same box: the 6 tets of one cell give the exact h range
         from .mesh import box_mesh
 
@@ -163,18 +166,32 @@ class BoxMesh:
         return float(np.prod(np.subtract(self.hi, self.lo)))
 
     def slab_layers(self, rank: int, world: int) -> tuple[int, int]:
-        if not 1 <= world <= self.nx:
-            raise ValueError("need 1 <= world <= nx cell layers")
-        return (self.nx * rank) // world, (self.nx * (rank + 1)) // world
+        """Cell layers [a, b) of `rank`: near-equal shares, cut at multiples of the x-blocking."""
+        nblk = -(-self.nx // self.xblock)
+        if not 1 <= world <= nblk:
+            raise ValueError("need 1 <= world <= number of x-blocks")
+        a, b = (nblk * rank) // world * self.xblock, (nblk * (rank + 1)) // world * self.xblock
+        return a, min(b, self.nx)
 
     def slab(self, rank: int, world: int) -> "BoxMesh":
         a, b = self.slab_layers(rank, world)
-        return BoxMesh(self.nx, self.ny, self.nz, self.lo, self.hi, a, b)
+        return BoxMesh(self.nx, self.ny, self.nz, self.lo, self.hi, a, b, self.xblock)
+
+    def local_element(self, cx, cy, cz, t, cx0: int | None = None):
+        """Element index (counted from layer cx0, default this slab's) of tet t of cell (cx, cy, cz)."""
+        cx, cy, cz = (np.asarray(v, dtype=np.int64) for v in (cx, cy, cz))
+        xb = self.xblock
+        s = cx // xb
+        ts = np.minimum(xb, self.nx - s * xb)
+        lin = s * xb * self.ny * self.nz + (cy * self.nz + cz) * ts + (cx - s * xb)
+        base = (self.cx0 if cx0 is None else cx0) * self.ny * self.nz
+        return (lin - base) * 6 + t
 
     def to_mesh(self) -> Mesh:
         from .mesh import box_mesh
 
-        return box_mesh(self.nx, self.ny, self.nz, self.lo, self.hi)
+        return box_mesh(self.nx, self.ny, self.nz, self.lo, self.hi, self.xblock)
 
     def __repr__(self):
-        return (f"BoxMesh({self.nx}x{self.ny}x{self.nz} cells, layers [{self.cx0}, {self.cx1}), K={self.K})")
+        return (f"BoxMesh({self.nx}x{self.ny}x{self.nz} cells, layers [{self.cx0}, {self.cx1}), xblock={self.xblock}, "
+                f"K={self.K})")

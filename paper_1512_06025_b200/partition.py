@@ -183,14 +183,15 @@ def box_halo_plan(box, world: int, rank: int) -> HaloPlan:
     a, b = box.slab_layers(rank, world)
     plane = box.ny * box.nz
     jk = np.arange(plane, dtype=np.int64)
+    cy, cz = jk // box.nz, jk % box.nz
     owner = [box.slab_layers(r, world) for r in range(world)]
 
     def owner_of(layer):
         return next(r for r, (x0, x1) in enumerate(owner) if x0 <= layer < x1)
 
     plan = HaloPlan(rank, world, 6 * a * plane, 6 * b * plane, None, None)
-    first = 6 * jk                                    # local elements of the first layer's cells
-    last = 6 * ((b - a - 1) * plane + jk)             # ... of the last layer's cells
+    first = box.local_element(np.full(plane, a), cy, cz, 0, a)       # tet 0 of the first layer's cells
+    last = box.local_element(np.full(plane, b - 1), cy, cz, 0, a)    # ... of the last layer's cells
     slot, halo = 0, []
     if a > 0:
         left = owner_of(a - 1)

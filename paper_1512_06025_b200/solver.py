@@ -155,7 +155,7 @@ class WaveSystem:
         if self._box:
             b = mesh
             lo, hi = (C.c_double * 3)(*b.lo), (C.c_double * 3)(*b.hi)
-            _lib.check(L.bbdg_ctx_set_box_mesh(ctx, b.nx, b.ny, b.nz, b.cx0, b.cx1, lo, hi, self._box_mat[0],
+            _lib.check(L.bbdg_ctx_set_box_mesh(ctx, b.nx, b.ny, b.nz, b.cx0, b.cx1, b.xblock, lo, hi, self._box_mat[0],
                                                self._box_mat[1], int(self._legacy), self._stream()),
                        "bbdg_ctx_set_box_mesh")
             self._upload_operators(ctx)

@@ -28,10 +28,11 @@ def records(sy):
     return geo, nbr, code
 
 
-@pytest.mark.parametrize("dims", [(1, 1, 1), (3, 2, 4), (5, 3, 2)])
+@pytest.mark.parametrize("dims,xblock", [((1, 1, 1), 1), ((3, 2, 4), 1), ((5, 3, 2), 1), ((5, 3, 2), 2),
+                                         ((7, 2, 3), 4)])
 @pytest.mark.parametrize("dname", ["f64", "f32"])
-def test_box_records_match_host_upload(dims, dname):
-    box = BoxMesh(*dims, lo=(-1.0, 0.0, 0.5), hi=(2.0, 1.0, 3.0))
+def test_box_records_match_host_upload(dims, xblock, dname):
+    box = BoxMesh(*dims, lo=(-1.0, 0.0, 0.5), hi=(2.0, 1.0, 3.0), xblock=xblock)
     m = box.to_mesh()
     ops = BernsteinRefOps.build(2)
     a = WaveSystem(m, ops, Materials.homogeneous(m.K, 2.0, 0.5), dtype=DT[dname])
@@ -44,9 +45,9 @@ def test_box_records_match_host_upload(dims, dname):
     assert box.h_min == pytest.approx(m.h_min, rel=1e-14) and box.K == m.K
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_box_slab_connectivity_matches_host_plan(world):
-    box = BoxMesh(6, 3, 2)
+@pytest.mark.parametrize("world,xblock", [(2, 1), (3, 1), (3, 2)])
+def test_box_slab_connectivity_matches_host_plan(world, xblock):
+    box = BoxMesh(6, 3, 2, xblock=xblock)
     m = box.to_mesh()
     plane = box.ny * box.nz
     ranges = [tuple(6 * x * plane for x in box.slab_layers(r, world)) for r in range(world)]
@@ -65,7 +66,7 @@ def test_box_slab_connectivity_matches_host_plan(world):
 def test_box_stage_matches_oracle(N, dname):
     from test_gpu_parity import stage_vs_oracle
 
-    box = BoxMesh(4, 3, 3)
+    box = BoxMesh(4, 3, 3, xblock=2)
     dtype = DT[dname]
     sy = WaveSystem(box, BernsteinRefOps.build(N), Materials.homogeneous(box.K), dtype=dtype, legacy_records=False)
     m = box.to_mesh()
@@ -77,15 +78,15 @@ def test_box_stage_matches_oracle(N, dname):
         sy.surface_rhs(__import__("paper_1512_06025_b200").FieldState(q, "bernstein"), "ell")
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_box_partitioned_stage_bitwise(P):
+@pytest.mark.parametrize("P,xblock", [(2, 1), (3, 1), (2, 3)])
+def test_box_partitioned_stage_bitwise(P, xblock):
     import torch
 
     from paper_1512_06025_b200.dist import DistWaveSystem
     from paper_1512_06025_b200.solver import RK4A, RK4B
     from test_partition import _FakeDist, _FakeWorld
 
-    box = BoxMesh(6, 4, 3)
+    box = BoxMesh(6, 4, 3, xblock=xblock)
     N = 5
     ops = BernsteinRefOps.build(N)
     mat = Materials.homogeneous(box.K_total)

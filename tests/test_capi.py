@@ -81,12 +81,13 @@ def test_round2_entry_points_validate_without_compute():
     assert lib.bbdg_ctx_create(3, 0, 0, 6 * 2 * 3 * 4, C.byref(ctx)) == 0
     lo, hi = (C.c_double * 3)(0, 0, 0), (C.c_double * 3)(1, 1, 1)
     try:
-        assert lib.bbdg_ctx_set_box_mesh(ctx, 0, 3, 4, 0, 0, lo, hi, 1.0, 1.0, 0, None) == 1      # nx < 1
-        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 1, 1, lo, hi, 1.0, 1.0, 0, None) == 1      # empty slab
-        assert lib.bbdg_ctx_set_box_mesh(ctx, 3, 3, 4, 0, 3, lo, hi, 1.0, 1.0, 0, None) == 1      # K mismatch
-        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, lo, hi, -1.0, 1.0, 0, None) == 1     # kappa <= 0
-        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, hi, lo, 1.0, 1.0, 0, None) == 1      # hi <= lo
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 0, 3, 4, 0, 0, 1, lo, hi, 1.0, 1.0, 0, None) == 1      # nx < 1
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 1, 1, 1, lo, hi, 1.0, 1.0, 0, None) == 1      # empty slab
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 3, 3, 4, 0, 3, 1, lo, hi, 1.0, 1.0, 0, None) == 1      # K mismatch
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, 1, lo, hi, -1.0, 1.0, 0, None) == 1     # kappa <= 0
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 2, 3, 4, 0, 2, 1, hi, lo, 1.0, 1.0, 0, None) == 1      # hi <= lo
         assert b"hi > lo" in lib.bbdg_last_error()
+        assert lib.bbdg_ctx_set_box_mesh(ctx, 4, 3, 1, 1, 3, 2, lo, hi, 1.0, 1.0, 0, None) == 1   # slab not on xblock
         assert lib.bbdg_step2(ctx, 16, 32, 16, 48, 0.1, 1, None) == 2                             # no geometry
     finally:
         lib.bbdg_ctx_destroy(ctx)

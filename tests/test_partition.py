@@ -73,13 +73,16 @@ def test_launch_ranges_cover_slab():
             assert inner[1] - inner[0] >= p.n_local // 4    # the middle slab overlaps the exchange
 
 
-@pytest.mark.parametrize("dims,world", [((4, 2, 3), 2), ((6, 3, 2), 3), ((5, 2, 2), 4), ((3, 1, 1), 3)])
-def test_box_halo_plan_matches_host_plan(dims, world):
-    """The closed-form plan of a device-built box slab (no host mesh) equals build_halo_plan's."""
+@pytest.mark.parametrize("dims,world,xblock", [((4, 2, 3), 2, 1), ((6, 3, 2), 3, 1), ((5, 2, 2), 4, 1),
+                                               ((3, 1, 1), 3, 1), ((8, 2, 3), 2, 2), ((6, 3, 2), 2, 3),
+                                               ((9, 2, 2), 2, 4)])
+def test_box_halo_plan_matches_host_plan(dims, world, xblock):
+    """The closed-form plan of a device-built box slab (no host mesh) equals build_halo_plan's, in the
+    reference element order and in the x-blocked order."""
     from paper_1512_06025_b200.mesh_device import BoxMesh
     from paper_1512_06025_b200.partition import box_halo_plan
 
-    box = BoxMesh(*dims)
+    box = BoxMesh(*dims, xblock=xblock)
     m = box.to_mesh()
     plane = dims[1] * dims[2]
     ranges = [tuple(6 * x * plane for x in box.slab_layers(r, world)) for r in range(world)]

@@ -144,8 +144,14 @@ class Clocks:
 
 # ---------------------------------------------------------------------- GPU arm
 # element order of the HBM-filling boxes: slabs of 4 x-layers, (y, z, x) inside a slab, so every neighbour
-# except those across a slab face lies within a few MB (L2) of its element (bbdg_ctx_set_box_mesh)
-XBLOCK = 4
+# except those across a slab face lies within a few MB (L2) of its element (bbdg_ctx_set_box_mesh).
+# Measured per order (fp32 stage frac, xblock 1 -> 4): N=1 0.81 -> 0.85, N=9 0.43 -> 0.46, but the
+# element-per-thread kernels' trace gather at N = 2, 3 prefers the reference order (0.56 -> 0.52).
+XBLOCK = None   # --xblock overrides the per-order choice
+
+
+def xblock_of(N):
+    return XBLOCK if XBLOCK else (1 if N in (2, 3) else 4)
 
 
 def fill_box(N, s, budget_bytes, ranks=1, xblock=1):
@@ -201,7 +207,7 @@ def run_dtype(args, dname, rank, world, dev, peak, clocks):
         torch.cuda.empty_cache()
         budget = args.fill * (total_mem - torch.cuda.memory_allocated(dev))
         if world == 1:
-            box = fill_box(N, s, budget, 1, XBLOCK)
+            box = fill_box(N, s, budget, 1, xblock_of(N))
             sy = WaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
                             legacy_records=False)
             K = box.K
@@ -209,10 +215,10 @@ def run_dtype(args, dname, rank, world, dev, peak, clocks):
             if args.strong:   # the 1-GPU mesh, split over the ranks (needs nx >= world layers)
                 from paper_1512_06025_b200.mesh_device import BoxMesh
 
-                one = fill_box(N, s, budget, 1, XBLOCK)
-                box = BoxMesh(max(one.nx, world * XBLOCK), one.ny, one.nz, xblock=XBLOCK)
+                one = fill_box(N, s, budget, 1, xblock_of(N))
+                box = BoxMesh(max(one.nx, world * xblock_of(N)), one.ny, one.nz, xblock=xblock_of(N))
             else:             # weak: an HBM-filling slab per rank
-                box = fill_box(N, s, budget, world, XBLOCK)
+                box = fill_box(N, s, budget, world, xblock_of(N))
             sy = DistWaveSystem(box, BernsteinRefOps.build(N), Materials(np.float64(1.0), np.float64(1.0)), dtype,
                                 rank, world, legacy_records=False)
             K = sy.K
@@ -231,7 +237,8 @@ def run_dtype(args, dname, rank, world, dev, peak, clocks):
         per_n[N] = t
         t_stage = t / args.steps
         ach = stage_bytes(N, s, K) / (t_stage * 1e-3) / 1e9
-        row = {"K": K, "box": [box.nx, box.ny, box.nz], "hbm_fraction": resident_bytes(N, s, K) / total_mem,
+        row = {"K": K, "box": [box.nx, box.ny, box.nz], "xblock": box.xblock,
+               "hbm_fraction": resident_bytes(N, s, K) / total_mem,
                "gdofs_stage": world * 4 * K * np_of(N) / (t_stage * 1e-3) / 1e9, "stage_ms": t_stage,
                "stage_gbs": ach, "stage_frac": ach / peak}
         if world == 1 and not args.quick:
@@ -437,8 +444,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodal", dest="nodal", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false", help="skip the host-state end-to-end leg")
+    ap.add_argument("--xblock", type=int, default=None, help="element order of the fill boxes (x-layers per slab)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global XBLOCK
+    if args.xblock:
+        XBLOCK = args.xblock
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     dnames = args.dtypes.split(",")
@@ -447,7 +458,7 @@ def main():
     scaling = "strong" if (args.strong and world > 1) else "weak"
     config = {"workload": WORKLOAD.format(orders=args.orders, lift=args.lift), "orders": orders, "lift": args.lift,
               "mesh": f"per order a device-built Kuhn box filling {args.fill:.2f} of free HBM, element order in "
-                      f"slabs of {XBLOCK} x-layers"
+                      f"slabs of {XBLOCK or 4} x-layers{'' if XBLOCK else ' (N = 2, 3: the reference x-slab order)'}"
                       + (f" per rank (x-layer slabs, {scaling} scaling)" if world > 1 else ""),
               "l2": "not flushed: every launch streams >= 1.4 GB (inputs larger than the 126 MB L2)",
               "materials": "homogeneous (kappa = rho = 1)",

@@ -251,6 +251,8 @@ template <typename T> static Params<T> make_params(const bbdg_ctx* c) {
   p.flux = static_cast<T*>(c->flux);
   p.bvol = c->bvol;
   p.blift = c->blift;
+  p.img_a = c->img_a;
+  p.img_l = c->img_l;
   return p;
 }
 
@@ -318,8 +320,29 @@ static int check_aligned(const void* a, const void* b = nullptr, const void* c =
   return (m & 15) ? set_error(BBDG_ERR_ARG, "state arrays must be 16-byte aligned") : BBDG_OK;
 }
 
+static int ensure_scratch(void** ptr, size_t bytes, const char* what) {
+  if (*ptr) return BBDG_OK;
+  cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return set_cuda_error(e, what);
+  }
+  return BBDG_OK;
+}
+
 template <typename T>
 static int run(bbdg_ctx* c, int op, int lift, Params<T>& p, void* stream, int basis = -1) {
+  if (lift == LIFT_BLOCKED && sizeof(T) == 4) {   // tcgen05 operand images (allocated on first use)
+    const TcDims d = tc_dims(c->N);
+    if (op != OP_SURFACE && !c->img_a) {
+      if (int rc = ensure_scratch(&c->img_a, tc_image_bytes(c->N, c->K, d.KV), "tcgen05 q image")) return rc;
+    }
+    if (op != OP_VOLUME && !c->img_l) {
+      if (int rc = ensure_scratch(&c->img_l, tc_image_bytes(c->N, c->K, d.KL), "tcgen05 flux image")) return rc;
+    }
+    p.img_a = c->img_a;
+    p.img_l = c->img_l;
+  }
   KernelEntry k = lookup(c->dtype, c->N, op, lift, basis < 0 ? c->basis : basis);
   if (!k.launch) return set_error(BBDG_ERR_UNSUPPORTED, "no kernel for this (op, lift, basis)");
   return k.launch(&p, static_cast<cudaStream_t>(stream), c->num_sms);
@@ -335,16 +358,6 @@ __global__ void stage_update_kernel(int64_t n, const T* __restrict__ q_in, T* __
     res[i] = r;
     q_out[i] = q_in[i] + b * r;
   }
-}
-
-static int ensure_scratch(void** ptr, size_t bytes, const char* what) {
-  if (*ptr) return BBDG_OK;
-  cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
-  if (e != cudaSuccess) {
-    *ptr = nullptr;
-    return set_cuda_error(e, what);
-  }
-  return BBDG_OK;
 }
 
 // The Bernstein "dense" lift (bernstein.py:332-347) on the tensor cores: the face fluxes
@@ -428,6 +441,8 @@ void bbdg_ctx_destroy(bbdg_ctx* c) {
   cudaFree(c->blift);
   cudaFree(c->flux);
   cudaFree(c->rhs_scratch);
+  cudaFree(c->img_a);
+  cudaFree(c->img_l);
   delete c;
 }
 

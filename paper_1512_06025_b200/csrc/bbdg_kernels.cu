@@ -118,7 +118,17 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
       if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute (nodal tc)");
       attr[dev].store(1, std::memory_order_release);
     }
-    const int64_t nsteps = (nl + LT::MT * LT::KE - 1) / (LT::MT * LT::KE);
+    if (!p.img_l || (OP != OP_SURFACE && !p.img_a))
+      return set_error(BBDG_ERR_UNSUPPORTED, "tcgen05 operand images not allocated");
+    const int64_t nsteps = (nl + LT::ST - 1) / LT::ST;
+    // tf32 hi / lo images of the element chunks in the UMMA layout (the kernel streams them with TMA)
+    const int pgrid = num_sms * 8;
+    if constexpr (OP != OP_SURFACE)
+      tc_pack_kernel<BBDG_N><<<pgrid, 256, 0, stream>>>(reinterpret_cast<const float*>(p.q + p.kbeg * LT::Np), p.K * LT::Np, LT::Np, LT::Np, LT::KV,
+                                                        nl, static_cast<float*>(p.img_a));
+    if constexpr (OP != OP_VOLUME)
+      tc_pack_kernel<BBDG_N><<<pgrid, 256, 0, stream>>>(reinterpret_cast<const float*>(p.flux), nl * 4 * LT::Nfp, 4 * LT::Nfp, 4 * LT::Nfp, LT::KL,
+                                                        nl, static_cast<float*>(p.img_l));
     kern<<<(unsigned)std::min<int64_t>(nsteps, num_sms), LT::threads, LT::total, stream>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal tcgen05 kernel launch");

@@ -28,22 +28,33 @@
 
 namespace bbdg {
 
-// tile geometry as a function of the degree (shared by the kernel and the host image builder)
+// tile geometry as a function of the degree (shared by the kernels and the host image builder)
 struct TcDims {
-  int Np, Nfp, KC, NB, NBLK, KV, KL, NV, SBO, BV_BYTES, BL_BYTES;
+  int Np, Nfp, KC, NB, NBLK, KV, KL, NV, SBO, BV_BYTES, BL_BYTES, MT;
 };
 __host__ __device__ constexpr TcDims tc_dims(int N) {
-  const int Np = (N + 1) * (N + 2) * (N + 3) / 6, Nfp = (N + 1) * (N + 2) / 2, KC = 8;
+  const int Np = (N + 1) * (N + 2) * (N + 3) / 6, Nfp = (N + 1) * (N + 2) / 2, KC = 16;
   const int NB = Np <= 16 ? 16 : (Np <= 32 ? 32 : 64);   // output nodes per block
+  // 128-row sub-tiles sharing each operator chunk: two while both accumulator sets of two sub-tiles
+  // fit the 512 TMEM columns twice over (double buffering), else one
+  const int MT = 2 * 2 * (4 * NB) <= 512 ? 2 : 1;
   return TcDims{Np, Nfp, KC, NB, (Np + NB - 1) / NB, (Np + KC - 1) / KC, (4 * Nfp + KC - 1) / KC, 3 * NB,
-                (KC / 4) * 128, 3 * NB * KC * 4, NB * KC * 4};
+                (KC / 4) * 128, 3 * NB * KC * 4, NB * KC * 4, MT};
+}
+
+// bytes of a packed element image of nl elements with nk K chunks (TcLayout: 64 elements per step,
+// both 128-row sub-tiles, tf32 hi and lo)
+inline size_t tc_image_bytes(int N, int64_t nl, int nk) {
+  const TcDims d = tc_dims(N);
+  return (size_t)((nl + 32 * d.MT - 1) / (32 * d.MT)) * nk * (size_t)(d.MT * 2 * 128 * d.KC * 4);
 }
 
 template <int N> struct TcLayout {
   static constexpr TcDims d = tc_dims(N);
   static constexpr int Np = d.Np, Nfp = d.Nfp;
-  static constexpr int MT = 2;                  // 128-row sub-tiles sharing each operator chunk
+  static constexpr int MT = d.MT;               // 128-row sub-tiles sharing each operator chunk
   static constexpr int KE = 32;                 // elements per sub-tile -> 128 rows
+  static constexpr int ST = MT * KE;            // elements per step
   static constexpr int M = 128;
   static constexpr int KC = d.KC;               // K per stage chunk (KC / 8 MMA k-steps)
   static constexpr int NB = d.NB, NBLK = d.NBLK;
@@ -51,31 +62,23 @@ template <int N> struct TcLayout {
   static constexpr int NV = d.NV;               // volume MMA N
   static constexpr int SBO = d.SBO;             // bytes between 8-row groups
   static constexpr int A_BYTES = M * KC * 4;    // one sub-tile, one of hi / lo
+  static constexpr int ABLK = MT * 2 * A_BYTES; // one packed element chunk (both sub-tiles, hi and lo)
   static constexpr int BV_BYTES = d.BV_BYTES;   // volume B chunk (hi or lo)
   static constexpr int BL_BYTES = d.BL_BYTES;
   static constexpr int B_BYTES = BV_BYTES > BL_BYTES ? BV_BYTES : BL_BYTES;
-  static constexpr int RAW_LD = KC + 4;         // padded fp32 row of the raw element chunk
-  static constexpr int B_OFF = MT * 2 * A_BYTES, RAW_OFF = B_OFF + 2 * B_BYTES;
-  static constexpr int STAGE = RAW_OFF + MT * M * RAW_LD * 4;
-  static constexpr int NS = (227 * 1024 - 128) / STAGE < 6 ? (227 * 1024 - 128) / STAGE : 6;   // pipeline depth
-  static constexpr int total = NS * STAGE + 128;                      // + mbarriers + TMEM slot
-  static constexpr int threads = 512;          // 16 warps: 4 per TMEM lane quarter in the epilogue
+  static constexpr int B_OFF = ABLK;
+  static constexpr int STAGE = B_OFF + 2 * B_BYTES;
+  static constexpr int NS = (227 * 1024 - 256) / STAGE < 8 ? (227 * 1024 - 256) / STAGE : 8;   // pipeline depth
+  static constexpr int total = NS * STAGE + 256;                      // + mbarriers + TMEM slot
+  static constexpr int threads = 192;           // warp 0 producer, warp 1 MMA issuer, warps 2-5 epilogue
   static constexpr int ACC = NV + NB;           // accumulator columns of one sub-tile
-  static constexpr int TM_COLS = MT * ACC <= 128 ? 128 : (MT * ACC <= 256 ? 256 : 512);
-  static_assert(MT * ACC <= 512, "accumulators exceed the TMEM columns");
-  static_assert(total <= 227 * 1024, "tcgen05 nodal tile does not fit in shared memory");
+  static constexpr int ABUF = MT * ACC;         // one accumulator buffer (double-buffered)
+  static constexpr int TM_COLS = 2 * ABUF <= 128 ? 128 : (2 * ABUF <= 256 ? 256 : 512);
+  static_assert(2 * ABUF <= 512, "accumulators exceed the TMEM columns");
+  static_assert(NS >= 2 && total <= 227 * 1024, "tcgen05 nodal tile does not fit in shared memory");
+  // packed element image: [step][kc][sub-tile][hi, lo][UMMA rows x KC]
+  static int64_t img_floats(int64_t nl, int nk) { return ((nl + ST - 1) / ST) * nk * (ABLK / 4); }
 };
-
-// wait until at most `newer` cp.async groups are still pending (wait_group needs an immediate)
-__device__ __forceinline__ void cp_async_wait_newer(int newer) {
-  switch (newer) {
-    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
-    case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
-  }
-}
 
 // byte offset of element (row, k) (k in the chunk) in the canonical no-swizzle K-major layout
 __host__ __device__ constexpr int umma_off(int sbo, int row, int k) {
@@ -112,20 +115,79 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-template <int N, int OP>
-__global__ void __launch_bounds__(TcLayout<N>::threads, 1) nodal_tc_kernel(const Params<float> p) {
+// Pack element rows (row 4e + F of a 32-element sub-tile; row data at src + F plane + e ld) into the
+// tcgen05 image: per (step, K chunk) one contiguous block [sub-tile][hi, lo][UMMA layout], the
+// tf32 hi / lo split done here once (zero rows past the range, zero K past kmax).
+template <int N>
+__global__ void __launch_bounds__(256) tc_pack_kernel(const float* __restrict__ src, int64_t plane, int ld, int kmax,
+                                                      int nk, int64_t nl, float* __restrict__ img) {
   using L = TcLayout<N>;
-  constexpr int Np = L::Np, Nfp = L::Nfp, KC = L::KC, NB = L::NB, NV = L::NV, MT = L::MT, NS = L::NS;
+  constexpr int KC = L::KC, UPR = KC / 4;   // 16-byte units per row and chunk
+  const int64_t nsteps = (nl + L::ST - 1) / L::ST;
+  const int64_t units = nsteps * nk * L::MT * L::M * UPR;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units; u += (int64_t)gridDim.x * blockDim.x) {
+    // u -> (step, kc, sub-tile, row, k-unit) with the unit fastest: reads run along a row
+    const int kq = (int)(u % UPR) * 4;
+    int64_t r = u / UPR;
+    const int row = (int)(r % L::M);
+    r /= L::M;
+    const int t = (int)(r % L::MT);
+    r /= L::MT;
+    const int kc = (int)(r % nk);
+    const int64_t step = r / nk;
+    const int64_t e = step * L::ST + t * L::KE + (row >> 2);
+    const int F = row & 3;
+    float x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = kc * KC + kq + j;
+      x[j] = (e < nl && k < kmax) ? src[F * plane + e * ld + k] : 0.f;
+    }
+    uint4 hi, lo;
+    uint32_t* h = &hi.x;
+    uint32_t* l = &lo.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      h[j] = tf32_bits(x[j]);
+      l[j] = tf32_bits(x[j] - __uint_as_float(h[j]));
+    }
+    unsigned char* blk = reinterpret_cast<unsigned char*>(img) + (step * nk + kc) * (int64_t)L::ABLK + t * 2 * L::A_BYTES;
+    const int off = umma_off(L::SBO, row, kq);
+    *reinterpret_cast<uint4*>(blk + off) = hi;
+    *reinterpret_cast<uint4*>(blk + L::A_BYTES + off) = lo;
+  }
+}
+
+// Warp-specialised tcgen05 GEMM with the fused nodal epilogue.  Warp 0 streams the packed element
+// chunks and the operator chunks into NS shared-memory stages with TMA bulk copies (full / empty
+// mbarriers per stage), warp 1 issues the 3xTF32 MMAs for both sub-tiles and commits each stage back
+// to the producer and each finished node block to the epilogue, warps 2-5 (one per TMEM lane
+// quarter) read the accumulators and run the chain rule / lift / LSRK epilogue while the producer
+// already streams the next block.
+template <int N, int OP>
+__global__ void __launch_bounds__(192, 1) nodal_tc_kernel(const Params<float> p) {
+  using L = TcLayout<N>;
+  constexpr int Np = L::Np, KC = L::KC, NB = L::NB, NV = L::NV, MT = L::MT, NS = L::NS;
   constexpr bool VOL = OP != OP_SURFACE, SURF = OP != OP_VOLUME;
-  extern __shared__ __align__(1024) unsigned char sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + NS * L::STAGE);
-  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(sm + NS * L::STAGE + 64);
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * L::STAGE);
+  uint64_t* empty = full + NS;
+  uint64_t* acc_full = empty + NS;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < NS; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(acc_full + i, 1);
+      mbar_init(acc_empty + i, 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tm_slot)),
                  "n"(L::TM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -136,148 +198,98 @@ __global__ void __launch_bounds__(TcLayout<N>::threads, 1) nodal_tc_kernel(const
   const uint32_t tmem = *tm_slot;
 
   const int64_t fs = p.K * Np, nl = p.kend - p.kbeg;
-  constexpr int ST = MT * L::KE;                 // elements per CTA step (MT sub-tiles)
-  const int64_t nsteps = (nl + ST - 1) / ST;
-  const float* bvh = static_cast<const float*>(p.bvol);                    // [blk][kc] chunks, hi then lo
-  const float* blh = static_cast<const float*>(p.blift);
-  constexpr int nchunk = (VOL ? L::KV : 0) + (SURF ? L::KL : 0);
-  constexpr int per_step = L::NBLK * nchunk;
+  const int64_t nsteps = (nl + L::ST - 1) / L::ST;
   const int64_t my_steps = blockIdx.x < nsteps ? (nsteps - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int nC = (int)(my_steps * per_step);   // this CTA's chunk sequence (step, node block, K chunk)
-  struct Chunk {
-    int64_t kt;   // first element of the step
-    int blk, ci, kc;
-    bool isvol;
-  };
-  auto decode = [&](int c) {   // 32-bit index math: divisions by compile-time constants
-    Chunk ch;
-    const int t = c / per_step;
-    const int r = c - t * per_step;
-    ch.blk = r / nchunk;
-    ch.ci = r - ch.blk * nchunk;
-    ch.kt = p.kbeg + ((int64_t)blockIdx.x + (int64_t)t * gridDim.x) * ST;
-    ch.isvol = VOL && ch.ci < (VOL ? L::KV : 0);
-    ch.kc = ch.isvol ? ch.ci : ch.ci - (VOL ? L::KV : 0);
-    return ch;
-  };
-  auto stage_ptr = [&](int st) { return sm + st * L::STAGE; };
-  // cp.async prefetch of a chunk: the element rows of both sub-tiles (fp32, zero-filled outside the
-  // mesh / K range) into the raw buffer, the operator image (hi, lo) straight into place
-  auto prefetch = [&](int c) {
-    const Chunk ch = decode(c);
-    unsigned char* sb = stage_ptr(c % NS);
-    const uint32_t raw = smem_u32(sb + L::RAW_OFF);
-    const int kmax = ch.isvol ? Np : 4 * Nfp;
-    if (!ch.isvol || Np % 4 == 0) {
-      // 16-byte rows (every flux row, and the state rows when Np = 0 mod 4): one cp.async per
-      // 4 values, the tail of a row zero-filled by the source size
-      for (int i = tid; i < MT * L::M * (KC / 4); i += L::threads) {
-        const int row = i / (KC / 4), k = (i - row * (KC / 4)) * 4, e = row >> 2, F = row & 3, kk = ch.kc * KC + k;
-        const int64_t ke = ch.kt + e;
-        const int nval = (ke < p.kend) ? (kmax - kk < 4 ? (kmax - kk > 0 ? kmax - kk : 0) : 4) : 0;
-        const float* src = nval == 0 ? p.q
-                           : ch.isvol ? p.q + F * fs + ke * Np + kk : p.flux + (F * nl + (ke - p.kbeg)) * 4 * Nfp + kk;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(raw + (row * L::RAW_LD + k) * 4),
-                     "l"(src), "r"(4 * nval)
-                     : "memory");
-      }
-    } else {
-      for (int i = tid; i < MT * L::M * KC; i += L::threads) {
-        const int row = i / KC, k = i - row * KC, e = row >> 2, F = row & 3, kk = ch.kc * KC + k;
-        const int64_t ke = ch.kt + e;
-        const bool ok = ke < p.kend && kk < kmax;
-        stage_cp<float>(raw + (row * L::RAW_LD + k) * 4, ok ? p.q + F * fs + ke * Np + kk : p.q, ok);
-      }
-    }
-    const int bytes = ch.isvol ? L::BV_BYTES : L::BL_BYTES;
-    const int nch = ch.isvol ? L::KV : L::KL;
-    const float* src = (ch.isvol ? bvh : blh) + ((int64_t)(ch.blk * nch + ch.kc) * 2) * (bytes / 4);
-    const uint32_t bh = smem_u32(sb + L::B_OFF), bl = bh + L::B_BYTES;
-    for (int i = tid; i < 2 * bytes / 16; i += L::threads)
-      cp_async<16>(i < bytes / 16 ? bh + i * 16 : bl + (i - bytes / 16) * 16, src + 4 * i);
-    cp_async_commit();
-  };
+  constexpr int nchunk = (VOL ? L::KV : 0) + (SURF ? L::KL : 0);
+  const int nC = (int)(my_steps * L::NBLK * nchunk);
+  const int nBlocks = (int)(my_steps * L::NBLK);
 
-  // prefetch distance NS - 2: the stage a prefetch overwrites was read by the MMAs of two chunks
-  // back, which have long completed -- the MMAs of the previous chunk keep running meanwhile
-  static_assert(NS >= 3, "pipeline needs three stages");
-  for (int c = 0; c < NS - 2 && c < nC; ++c) prefetch(c);
-  for (int c = 0; c < nC; ++c) {
-    const Chunk ch = decode(c);
-    const int st = c % NS;
-    unsigned char* sbase = stage_ptr(st);
-    const float* araw = reinterpret_cast<const float*>(sbase + L::RAW_OFF);
-    // this chunk's copies landed (the newer prefetches may stay in flight)
-    {
-      // groups committed after chunk c's: min(NS - 2, nC - 1 - c)
-      const int newer = (nC - 1 - c) < NS - 3 ? (nC - 1 - c) : NS - 3;
-      cp_async_wait_newer(newer);
-    }
-    __syncthreads();
-    // ---- split the element rows into tf32 hi / lo in the UMMA layout (consecutive threads:
-    // consecutive 16-byte rows of a core matrix; raw rows padded -> both sides conflict-free)
-    for (int u = tid; u < MT * L::M * (KC / 4); u += L::threads) {
-      const int row = (u / (8 * (KC / 4))) * 8 + (u & 7), kq = ((u >> 3) % (KC / 4)) * 4;
-      const float4 x4 = *reinterpret_cast<const float4*>(araw + row * L::RAW_LD + kq);
-      const float x[4] = {x4.x, x4.y, x4.z, x4.w};
-      uint4 hi, lo;
-      uint32_t* h = &hi.x;
-      uint32_t* l = &lo.x;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        h[j] = tf32_bits(x[j]);
-        l[j] = tf32_bits(x[j] - __uint_as_float(h[j]));
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const float* bvh = static_cast<const float*>(p.bvol);
+      const float* blh = static_cast<const float*>(p.blift);
+      // an element chunk is read once per node block: keep it in L2 until the last block's read
+      const uint64_t keep = l2_policy(true), drop = l2_policy(false);
+      for (int c = 0; c < nC; ++c) {
+        const int st = c % NS;
+        if (c >= NS) mbar_wait(empty + st, (uint32_t)(((c / NS) - 1) & 1));
+        const int step_i = c / (L::NBLK * nchunk), r = c - step_i * (L::NBLK * nchunk);
+        const int blk = r / nchunk, ci = r - blk * nchunk;
+        const bool isvol = VOL && ci < (VOL ? L::KV : 0);
+        const int kc = isvol ? ci : ci - (VOL ? L::KV : 0);
+        const int64_t step = blockIdx.x + (int64_t)step_i * gridDim.x;
+        const float* asrc = static_cast<const float*>(isvol ? p.img_a : p.img_l) +
+                            (step * (isvol ? L::KV : L::KL) + kc) * (int64_t)(L::ABLK / 4);
+        const int bbytes = isvol ? L::BV_BYTES : L::BL_BYTES;
+        const float* bsrc = (isvol ? bvh : blh) + ((int64_t)(blk * (isvol ? L::KV : L::KL) + kc) * 2) * (bbytes / 4);
+        unsigned char* sb = sm + st * L::STAGE;
+        mbar_expect_tx(full + st, L::ABLK + 2 * bbytes);
+        tma_bulk_g2s_hint(sb, asrc, L::ABLK, full + st, blk == L::NBLK - 1 ? drop : keep);
+        tma_bulk_g2s_hint(sb + L::B_OFF, bsrc, 2 * bbytes, full + st, keep);
       }
-      const int t = row >> 7, off = t * 2 * L::A_BYTES + umma_off(L::SBO, row & 127, kq);
-      *reinterpret_cast<uint4*>(sbase + off) = hi;
-      *reinterpret_cast<uint4*>(sbase + off + L::A_BYTES) = lo;
     }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t bh = smem_u32(sbase + L::B_OFF), bl = bh + L::B_BYTES;
-      const uint32_t idesc = ch.isvol ? umma_idesc_tf32(128, NV) : umma_idesc_tf32(128, NB);
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int blk_i = 0;
+      for (int c = 0; c < nC; ++c) {
+        const int st = c % NS;
+        const int r = c % (L::NBLK * nchunk), ci = r % nchunk;
+        const bool isvol = VOL && ci < (VOL ? L::KV : 0);
+        const int kc = isvol ? ci : ci - (VOL ? L::KV : 0);
+        const int buf = blk_i & 1;
+        // the buffer's previous node block has been drained by the epilogue
+        if (ci == 0 && blk_i >= 2) mbar_wait(acc_empty + buf, (uint32_t)(((blk_i >> 1) - 1) & 1));
+        mbar_wait(full + st, (uint32_t)((c / NS) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        unsigned char* sb = sm + st * L::STAGE;
+        const uint32_t bh = smem_u32(sb + L::B_OFF), bl = bh + (isvol ? L::BV_BYTES : L::BL_BYTES);
+        const uint32_t idesc = isvol ? umma_idesc_tf32(128, NV) : umma_idesc_tf32(128, NB);
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const uint32_t ah = smem_u32(sbase + t * 2 * L::A_BYTES), al = ah + L::A_BYTES;
-        const uint32_t d = tmem + t * L::ACC + (ch.isvol ? 0 : NV);
+        for (int t = 0; t < MT; ++t) {
+          const uint32_t ah = smem_u32(sb + t * 2 * L::A_BYTES), al = ah + L::A_BYTES;
+          const uint32_t d = tmem + buf * L::ABUF + t * L::ACC + (isvol ? 0 : NV);
 #pragma unroll
-        for (int ks = 0; ks < KC / 8; ++ks) {
-          const uint32_t ko = ks * 256;   // two 16-byte K units per k-step
-          const uint64_t dah = umma_desc(ah + ko, 128, L::SBO), dal = umma_desc(al + ko, 128, L::SBO);
-          const uint64_t dbh = umma_desc(bh + ko, 128, L::SBO), dbl = umma_desc(bl + ko, 128, L::SBO);
-          umma_tf32(d, dal, dbh, idesc, (ch.kc | ks) != 0);
-          umma_tf32(d, dah, dbl, idesc, 1);
-          umma_tf32(d, dah, dbh, idesc, 1);
+          for (int ks = 0; ks < KC / 8; ++ks) {
+            const uint32_t ko = ks * 256;   // two 16-byte K units per k-step
+            const uint64_t dah = umma_desc(ah + ko, 128, L::SBO), dal = umma_desc(al + ko, 128, L::SBO);
+            const uint64_t dbh = umma_desc(bh + ko, 128, L::SBO), dbl = umma_desc(bl + ko, 128, L::SBO);
+            umma_tf32(d, dal, dbh, idesc, (kc | ks) != 0);
+            umma_tf32(d, dah, dbl, idesc, 1);
+            umma_tf32(d, dah, dbh, idesc, 1);
+          }
+        }
+        umma_commit(empty + st);                      // the stage is free once these MMAs complete
+        if (ci == nchunk - 1) {
+          umma_commit(acc_full + buf);                // the node block's accumulators are complete
+          ++blk_i;
         }
       }
-      umma_commit(bars + st);
     }
-    if (c + NS - 2 < nC) {
-      // the stage of chunk c + NS - 2 was last read by chunk c - 2's MMAs
-      if (c >= 2) mbar_wait(bars + (c - 2) % NS, (uint32_t)(((c - 2) / NS) & 1));
-      prefetch(c + NS - 2);
-    }
-    if (ch.ci == nchunk - 1) {
-      // ---- epilogue of this node block: all accumulators complete
-      mbar_wait(bars + st, (uint32_t)((c / NS) & 1));
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-5)
+    const int wq = warp & 3;                          // TMEM lane quarter of this warp
+    const int row = wq * 32 + lane, F = row & 3, base = lane & ~3;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    for (int b = 0; b < nBlocks; ++b) {
+      const int64_t step = blockIdx.x + (int64_t)(b / L::NBLK) * gridDim.x;
+      const int blk = b % L::NBLK;
+      const int buf = b & 1;
+      mbar_wait(acc_full + buf, (uint32_t)((b >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const int wq = warp & 3, half = warp >> 2;   // TMEM lane quarter, column quarter
-      const int row = wq * 32 + lane, F = row & 3, base = lane & ~3;
-      const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
 #pragma unroll 1
       for (int t = 0; t < MT; ++t) {
-        const int64_t k = ch.kt + t * L::KE + (row >> 2);
+        const int64_t k = p.kbeg + step * L::ST + t * L::KE + (row >> 2);
         const bool okr = k < p.kend;
-        const float* gv = p.geo_vol + (okr ? k : ch.kt) * kGeoVol;
+        const float* gv = p.geo_vol + (okr ? k : p.kbeg) * kGeoVol;
         float G[9];
 #pragma unroll
         for (int j = 0; j < 9; ++j) G[j] = gv[j];
         const float kap = gv[9], irho = gv[10];
-        const uint32_t tv = tmem + t * L::ACC + lane_off, tl = tv + NV;
+        const uint32_t tv = tmem + buf * L::ABUF + t * L::ACC + lane_off, tl = tv + NV;
 #pragma unroll 1
-        for (int a0 = 16 * half; a0 < NB; a0 += 16 * (L::threads / 128)) {
+        for (int a0 = 0; a0 < NB; a0 += 16) {
           uint32_t gr[16], gs[16], gt[16], li[16];
           if constexpr (VOL) {
             tm_ld<16>(tv + a0, gr);
@@ -288,7 +300,7 @@ __global__ void __launch_bounds__(TcLayout<N>::threads, 1) nodal_tc_kernel(const
           tm_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int a = ch.blk * NB + a0 + j;
+            const int a = blk * NB + a0 + j;
             float r = 0.f;
             if constexpr (VOL) {
               const float g0 = __uint_as_float(gr[j]), g1 = __uint_as_float(gs[j]), g2 = __uint_as_float(gt[j]);
@@ -330,12 +342,13 @@ __global__ void __launch_bounds__(TcLayout<N>::threads, 1) nodal_tc_kernel(const
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncthreads();   // accumulators read: the next block's MMAs may overwrite them
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + buf);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(L::TM_COLS));
 }
 

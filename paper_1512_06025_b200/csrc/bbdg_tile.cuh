@@ -58,6 +58,8 @@ template <typename T> struct Params {
   T* flux;               // nodal blocked path: (4, kend - kbeg, 4 Nfp) face fluxes (context-owned)
   const void* bvol;      // nodal blocked path: D_m^T MMA fragments (bbdg_nodal.cuh)
   const void* blift;     // nodal blocked path: L^T MMA fragments
+  void* img_a;           // fp32 tcgen05 path: packed element chunks of q (bbdg_tc.cuh, context-owned)
+  void* img_l;           // fp32 tcgen05 path: packed element chunks of the face fluxes
 };
 
 template <typename T> struct alignas(4 * sizeof(T)) V4 {

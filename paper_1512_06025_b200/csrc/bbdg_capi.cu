@@ -289,7 +289,7 @@ static int check_lift(const bbdg_ctx* c, int& lift, bool surf) {
     // WaveSystem forces "dense" for the nodal basis (solver.py:168-169); BLOCKED selects the
     // tensor-core (EPT) kernels for the same arithmetic
     if (lift == BBDG_LIFT_BLOCKED) {
-      if (!c->bvol || !c->blift || !c->flux)
+      if (!c->bvol || !c->blift || (c->dtype == BBDG_F64 && !c->flux))
         return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded (set_nodal_ops + set_lift_tables)");
       lift = LIFT_BLOCKED;
       return BBDG_OK;
@@ -334,11 +334,16 @@ template <typename T>
 static int run(bbdg_ctx* c, int op, int lift, Params<T>& p, void* stream, int basis = -1) {
   if (lift == LIFT_BLOCKED && sizeof(T) == 4) {   // tcgen05 operand images (allocated on first use)
     const TcDims d = tc_dims(c->N);
+    // zero-filled once: the K padding of the images is never written (the kernels write real entries only)
     if (op != OP_SURFACE && !c->img_a) {
       if (int rc = ensure_scratch(&c->img_a, tc_image_bytes(c->N, c->K, d.KV), "tcgen05 q image")) return rc;
+      cudaMemset(c->img_a, 0, tc_image_bytes(c->N, c->K, d.KV));
+      cudaDeviceSynchronize();   // one-time: ordered before any stream's use
     }
     if (op != OP_VOLUME && !c->img_l) {
       if (int rc = ensure_scratch(&c->img_l, tc_image_bytes(c->N, c->K, d.KL), "tcgen05 flux image")) return rc;
+      cudaMemset(c->img_l, 0, tc_image_bytes(c->N, c->K, d.KL));
+      cudaDeviceSynchronize();
     }
     p.img_a = c->img_a;
     p.img_l = c->img_l;
@@ -370,7 +375,9 @@ template <typename T>
 static int bb_dense_tc(bbdg_ctx* c, int op, const void* q, void* out, void* res, double a, double b, double dt,
                        int accumulate, void* stream) {
   const size_t sz = sizeof(T);
-  if (int rc = ensure_scratch(&c->flux, (size_t)4 * c->K * 4 * c->Nfp * sz, "dense-lift flux scratch")) return rc;
+  if (sz == 8) {   // fp64 DMMA path: flux round trip (fp32 writes the tcgen05 flux image directly)
+    if (int rc = ensure_scratch(&c->flux, (size_t)4 * c->K * 4 * c->Nfp * sz, "dense-lift flux scratch")) return rc;
+  }
   Params<T> p = make_params<T>(c);
   p.q = static_cast<const T*>(q);
   T* rhs = static_cast<T*>(op == OP_STAGE ? nullptr : out);
@@ -496,7 +503,7 @@ int bbdg_ctx_set_lift_tables(bbdg_ctx* c, const int32_t* el_cols, const double* 
       } else {
         c->blift = upload(mma_fragments<double>(m, 1, Np, 4 * Nfp), &rc);
       }
-      if (c->basis == BBDG_BASIS_NODAL) {
+      if (c->basis == BBDG_BASIS_NODAL && c->dtype == BBDG_F64) {
         const size_t fb = (size_t)4 * c->K * 4 * Nfp * (c->dtype == BBDG_F32 ? 4 : 8);
         cudaError_t e = cudaMalloc(&c->flux, std::max<size_t>(fb, 16));
         if (e != cudaSuccess) {

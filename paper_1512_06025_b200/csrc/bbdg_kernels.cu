@@ -100,9 +100,9 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
   const Params<T>& p = *static_cast<const Params<T>*>(vp);
   const int64_t nl = p.kend - p.kbeg;
   if (nl == 0) return BBDG_OK;
-  if ((OP != OP_SURFACE && !p.bvol) || !p.blift || !p.flux)
+  if ((OP != OP_SURFACE && !p.bvol) || !p.blift || (sizeof(T) == 8 && !p.flux))
     return set_error(BBDG_ERR_UNSUPPORTED, "nodal MMA fragments not uploaded");
-  if constexpr (OP != OP_VOLUME) {
+  if constexpr (OP != OP_VOLUME && sizeof(T) == 8) {
     const int64_t n = nl * 4 * Dims<BBDG_N>::Nfp;
     const int64_t grid = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 8);
     nodal_flux_kernel<T, BBDG_N><<<(unsigned)grid, 256, 0, stream>>>(p);
@@ -126,10 +126,13 @@ template <int OP> int launch_nodal(const void* vp, cudaStream_t stream, int num_
     if constexpr (OP != OP_SURFACE)
       tc_pack_kernel<BBDG_N><<<pgrid, 256, 0, stream>>>(reinterpret_cast<const float*>(p.q + p.kbeg * LT::Np), p.K * LT::Np, LT::Np, LT::Np, LT::KV,
                                                         nl, static_cast<float*>(p.img_a));
-    if constexpr (OP != OP_VOLUME)
-      tc_pack_kernel<BBDG_N><<<pgrid, 256, 0, stream>>>(reinterpret_cast<const float*>(p.flux), nl * 4 * LT::Nfp, 4 * LT::Nfp, 4 * LT::Nfp, LT::KL,
-                                                        nl, static_cast<float*>(p.img_l));
-    kern<<<(unsigned)std::min<int64_t>(nsteps, num_sms), LT::threads, LT::total, stream>>>(p);
+    if constexpr (OP != OP_VOLUME) {
+      const int64_t n = nl * 4 * LT::Nfp;
+      tc_flux_kernel<BBDG_N><<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 8), 256, 0, stream>>>(
+          reinterpret_cast<const Params<float>&>(p));
+    }
+    kern<<<(unsigned)std::min<int64_t>(nsteps, num_sms), LT::threads, LT::total, stream>>>(
+        reinterpret_cast<const Params<float>&>(p));
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BBDG_OK : set_cuda_error(e, "nodal tcgen05 kernel launch");
   }

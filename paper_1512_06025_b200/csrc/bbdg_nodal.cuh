@@ -115,60 +115,73 @@ template <typename T, int N> struct NodalLayout {
   static constexpr int total = (sf + 4 * ET * LF) * (int)sizeof(T);
 };
 
+// Face flux of the nodal path at face point fm = f Nfp + m of element k:
+// fl = (Fp, n1 Fu, n2 Fu, n3 Fu)   (solver.py:166-185)
+template <typename T, int N>
+__device__ __forceinline__ void nodal_face_flux(const Params<T>& p, int64_t k, int fm, T fl[4]) {
+  constexpr int Np = Dims<N>::Np, Nfp = Dims<N>::Nfp;
+  const int64_t fs = p.K * Np;
+  const int f = fm / Nfp, m = fm - f * Nfp;
+  int b0, b1;
+  decode2(N, m, b0, b1);
+  const int b[3] = {b0, b1, N - b0 - b1};
+  int a[4], s = 0;
+  for (int v = 0; v < 4; ++v) a[v] = (v == f) ? 0 : b[s++];
+  const int pos = pos3(N, a[0], a[1], a[2]);
+  const T* gs = p.geo_surf + k * kGeoSurf + f * 6;
+  const int cd = (p.code[k] >> (8 * f)) & 0xff;
+  const bool bnd = (cd >> 5) & 1;
+  T loc[4], nb[4];
+#pragma unroll
+  for (int F = 0; F < 4; ++F) loc[F] = p.q[F * fs + k * Np + pos];
+  if (bnd) {
+#pragma unroll
+    for (int F = 0; F < 4; ++F) nb[F] = loc[F];
+  } else {
+    // neighbour point: the shared face's vertex permutation (multiindex.PERMS3)
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    const int s2 = (cd >> 2) & 7, f2 = cd & 3;
+    int c[3];
+    for (int kk = 0; kk < 3; ++kk) c[perms[s2][kk]] = b[kk];
+    const int m2 = pos2(N, c[0], c[1]);
+    const int64_t k2 = p.nbr[k * 4 + f];
+    if ((cd >> 6) & 1) {
+#pragma unroll
+      for (int F = 0; F < 4; ++F) nb[F] = p.halo[(F * p.nhalo + k2) * Nfp + m2];
+    } else {
+      int a2[4], s3 = 0;
+      for (int v = 0; v < 4; ++v) a2[v] = (v == f2) ? 0 : c[s3++];
+      const int pos2n = pos3(N, a2[0], a2[1], a2[2]);
+#pragma unroll
+      for (int F = 0; F < 4; ++F) nb[F] = p.q[F * fs + k2 * Np + pos2n];
+    }
+  }
+  const T jp = bnd ? T(-2) * loc[0] : nb[0] - loc[0];
+  const T jun = gs[0] * (nb[1] - loc[1]) + gs[1] * (nb[2] - loc[2]) + gs[2] * (nb[3] - loc[3]);
+  const T Fp = T(0.5) * (gs[4] * jp - jun) * gs[3];
+  const T Fu = T(0.5) * (gs[5] * jun - jp) * gs[3];
+  fl[0] = Fp;
+  fl[1] = gs[0] * Fu;
+  fl[2] = gs[1] * Fu;
+  fl[3] = gs[2] * Fu;
+}
+
 // Face fluxes of the nodal path, one thread per (element, face, point):
-// flux[F][k][f Nfp + m] = (Fp, n1 Fu, n2 Fu, n3 Fu)   (solver.py:166-185)
+// flux[F][k][f Nfp + m] = (Fp, n1 Fu, n2 Fu, n3 Fu)
 template <typename T, int N>
 __global__ void __launch_bounds__(256) nodal_flux_kernel(const Params<T> p) {
-  constexpr int Np = Dims<N>::Np, Nfp = Dims<N>::Nfp;
-  const int64_t fs = p.K * Np, nl = p.kend - p.kbeg;
+  constexpr int Nfp = Dims<N>::Nfp;
+  const int64_t nl = p.kend - p.kbeg;
   const int64_t total = nl * 4 * Nfp;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = p.kbeg + x / (4 * Nfp);
-    const int fm = (int)(x % (4 * Nfp)), f = fm / Nfp, m = fm - f * Nfp;
-    int b0, b1;
-    decode2(N, m, b0, b1);
-    const int b[3] = {b0, b1, N - b0 - b1};
-    int a[4], s = 0;
-    for (int v = 0; v < 4; ++v) a[v] = (v == f) ? 0 : b[s++];
-    const int pos = pos3(N, a[0], a[1], a[2]);
-    const T* gs = p.geo_surf + k * kGeoSurf + f * 6;
-    const int cd = (p.code[k] >> (8 * f)) & 0xff;
-    const bool bnd = (cd >> 5) & 1;
-    T loc[4], nb[4];
-#pragma unroll
-    for (int F = 0; F < 4; ++F) loc[F] = p.q[F * fs + k * Np + pos];
-    if (bnd) {
-#pragma unroll
-      for (int F = 0; F < 4; ++F) nb[F] = loc[F];
-    } else {
-      // neighbour point: the shared face's vertex permutation (multiindex.PERMS3)
-      const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-      const int s2 = (cd >> 2) & 7, f2 = cd & 3;
-      int c[3];
-      for (int kk = 0; kk < 3; ++kk) c[perms[s2][kk]] = b[kk];
-      const int m2 = pos2(N, c[0], c[1]);
-      const int64_t k2 = p.nbr[k * 4 + f];
-      if ((cd >> 6) & 1) {
-#pragma unroll
-        for (int F = 0; F < 4; ++F) nb[F] = p.halo[(F * p.nhalo + k2) * Nfp + m2];
-      } else {
-        int a2[4], s3 = 0;
-        for (int v = 0; v < 4; ++v) a2[v] = (v == f2) ? 0 : c[s3++];
-        const int pos2n = pos3(N, a2[0], a2[1], a2[2]);
-#pragma unroll
-        for (int F = 0; F < 4; ++F) nb[F] = p.q[F * fs + k2 * Np + pos2n];
-      }
-    }
-    const T jp = bnd ? T(-2) * loc[0] : nb[0] - loc[0];
-    const T jun = gs[0] * (nb[1] - loc[1]) + gs[1] * (nb[2] - loc[2]) + gs[2] * (nb[3] - loc[3]);
-    const T Fp = T(0.5) * (gs[4] * jp - jun) * gs[3];
-    const T Fu = T(0.5) * (gs[5] * jun - jp) * gs[3];
-    T* o = p.flux + (k - p.kbeg) * 4 * Nfp + fm;
+    const int64_t e = x / (4 * Nfp);
+    const int fm = (int)(x - e * 4 * Nfp);
+    T fl[4];
+    nodal_face_flux<T, N>(p, p.kbeg + e, fm, fl);
+    T* o = p.flux + e * 4 * Nfp + fm;
     const int64_t ps = nl * 4 * Nfp;
-    o[0] = Fp;
-    o[ps] = gs[0] * Fu;
-    o[2 * ps] = gs[1] * Fu;
-    o[3 * ps] = gs[2] * Fu;
+#pragma unroll
+    for (int F = 0; F < 4; ++F) o[F * ps] = fl[F];
   }
 }
 

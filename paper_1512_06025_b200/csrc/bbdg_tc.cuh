@@ -158,6 +158,34 @@ __global__ void __launch_bounds__(256) tc_pack_kernel(const float* __restrict__ 
   }
 }
 
+// The nodal face fluxes written straight into the tcgen05 flux image (tf32 hi / lo in the UMMA
+// layout, row 4 e + F of the element's sub-tile, column f Nfp + m): no flux round trip through HBM.
+// Column padding of the image stays zero from its allocation.
+template <int N>
+__global__ void __launch_bounds__(256) tc_flux_kernel(const Params<float> p) {
+  using L = TcLayout<N>;
+  constexpr int Nfp = L::Nfp;
+  const int64_t nl = p.kend - p.kbeg;
+  const int64_t total = nl * 4 * Nfp;
+  unsigned char* img = static_cast<unsigned char*>(p.img_l);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = x / (4 * Nfp);
+    const int fm = (int)(x - e * 4 * Nfp);
+    float fl[4];
+    nodal_face_flux<float, N>(p, p.kbeg + e, fm, fl);
+    const int64_t step = e / L::ST;
+    const int el = (int)(e - step * L::ST), t = el / L::KE, kc = fm / L::KC;
+    unsigned char* blk = img + (step * L::KL + kc) * (int64_t)L::ABLK + t * 2 * L::A_BYTES;
+#pragma unroll
+    for (int F = 0; F < 4; ++F) {
+      const int off = umma_off(L::SBO, 4 * (el - t * L::KE) + F, fm - kc * L::KC);
+      const uint32_t h = tf32_bits(fl[F]);
+      *reinterpret_cast<uint32_t*>(blk + off) = h;
+      *reinterpret_cast<uint32_t*>(blk + L::A_BYTES + off) = tf32_bits(fl[F] - __uint_as_float(h));
+    }
+  }
+}
+
 // Warp-specialised tcgen05 GEMM with the fused nodal epilogue.  Warp 0 streams the packed element
 // chunks and the operator chunks into NS shared-memory stages with TMA bulk copies (full / empty
 // mbarriers per stage), warp 1 issues the 3xTF32 MMAs for both sub-tiles and commits each stage back
@@ -283,11 +311,16 @@ __global__ void __launch_bounds__(192, 1) nodal_tc_kernel(const Params<float> p)
         const int64_t k = p.kbeg + step * L::ST + t * L::KE + (row >> 2);
         const bool okr = k < p.kend;
         const float* gv = p.geo_vol + (okr ? k : p.kbeg) * kGeoVol;
-        float G[9];
+        // chain-rule coefficients of this row's field: u_i rows (F = i + 1) use column i of the
+        // metric, G[3 m + i] (m = r, s, t); the p row uses none (its share of the divergence is 0)
+        float Gc[3];
 #pragma unroll
-        for (int j = 0; j < 9; ++j) G[j] = gv[j];
-        const float kap = gv[9], irho = gv[10];
+        for (int m = 0; m < 3; ++m) Gc[m] = F == 0 ? 0.f : gv[3 * m + (F == 0 ? 0 : F - 1)];
+        const float mat = F == 0 ? gv[9] : gv[10];   // kappa for p, 1 / rho for u_i
         const uint32_t tv = tmem + buf * L::ABUF + t * L::ACC + lane_off, tl = tv + NV;
+        float* outp = p.out + F * fs + k * Np;
+        float* resp = OP == OP_STAGE ? p.res + F * fs + k * Np : nullptr;
+        const float* qp = OP == OP_STAGE ? p.q + F * fs + k * Np : nullptr;
 #pragma unroll 1
         for (int a0 = 0; a0 < NB; a0 += 16) {
           uint32_t gr[16], gs[16], gt[16], li[16];
@@ -298,44 +331,62 @@ __global__ void __launch_bounds__(192, 1) nodal_tc_kernel(const Params<float> p)
           }
           if constexpr (SURF) tm_ld<16>(tl + a0, li);
           tm_wait_ld();
+          float r[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int a = blk * NB + a0 + j;
-            float r = 0.f;
+            float x = 0.f;
             if constexpr (VOL) {
-              const float g0 = __uint_as_float(gr[j]), g1 = __uint_as_float(gs[j]), g2 = __uint_as_float(gt[j]);
-              // the p row's derivatives (lane base) and the u rows' (base + 1..3) of this element
-              const float p0 = __shfl_sync(0xffffffffu, g0, base), p1 = __shfl_sync(0xffffffffu, g1, base),
-                          p2 = __shfl_sync(0xffffffffu, g2, base);
-              float div = 0.f;
+              const float d0 = __uint_as_float(gr[j]), d1 = __uint_as_float(gs[j]), d2 = __uint_as_float(gt[j]);
+              // u_i rows: own share of div u, and grad_i p from the p row's derivatives (lane base)
+              const float c = Gc[0] * d0 + Gc[1] * d1 + Gc[2] * d2;
+              const float p0 = __shfl_sync(0xffffffffu, d0, base), p1 = __shfl_sync(0xffffffffu, d1, base),
+                          p2 = __shfl_sync(0xffffffffu, d2, base);
+              const float g = Gc[0] * p0 + Gc[1] * p1 + Gc[2] * p2;
+              float dv = c + __shfl_xor_sync(0xffffffffu, c, 1);
+              dv += __shfl_xor_sync(0xffffffffu, dv, 2);   // div u over the element's four rows
+              x = F == 0 ? dv : g;
+            }
+            // rhs = material (lift - chain rule): -kappa div u + kappa L f_p, -grad_i p / rho + L f_ui / rho
+            r[j] = SURF ? mat * (__uint_as_float(li[j]) - x) : -mat * x;
+          }
+          const int a = blk * NB + a0;
+          if (!okr || a >= Np) continue;
+          if (Np % 4 == 0 && a + 16 <= Np) {   // 16-byte aligned rows: vector accesses
 #pragma unroll
-              for (int i = 0; i < 3; ++i) {
-                const float u0 = __shfl_sync(0xffffffffu, g0, base + 1 + i);
-                const float u1 = __shfl_sync(0xffffffffu, g1, base + 1 + i);
-                const float u2 = __shfl_sync(0xffffffffu, g2, base + 1 + i);
-                div += G[i] * u0 + G[3 + i] * u1 + G[6 + i] * u2;
-              }
-              if (F == 0) {
-                r = -kap * div;
-              } else {
-                const int i = F - 1;
-                r = -irho * (G[i] * p0 + G[3 + i] * p1 + G[6 + i] * p2);
-              }
-            }
-            if constexpr (SURF) {
-              const float s = (F == 0 ? kap : irho) * __uint_as_float(li[j]);
-              r = VOL ? r + s : s;
-            }
-            if (okr && a < Np) {
-              const int64_t o = F * fs + k * Np + a;
+            for (int j = 0; j < 16; j += 4) {
+              float4 v = make_float4(r[j], r[j + 1], r[j + 2], r[j + 3]);
               if constexpr (OP == OP_STAGE) {
-                float x = p.res[o] * p.rk_a;
-                x = x + p.dt * r;
-                p.res[o] = x;
-                p.out[o] = p.q[o] + p.rk_b * x;
+                float4 rs = *reinterpret_cast<const float4*>(resp + a + j);
+                const float4 qv = *reinterpret_cast<const float4*>(qp + a + j);
+                rs.x = rs.x * p.rk_a + p.dt * v.x;
+                rs.y = rs.y * p.rk_a + p.dt * v.y;
+                rs.z = rs.z * p.rk_a + p.dt * v.z;
+                rs.w = rs.w * p.rk_a + p.dt * v.w;
+                *reinterpret_cast<float4*>(resp + a + j) = rs;
+                *reinterpret_cast<float4*>(outp + a + j) =
+                    make_float4(qv.x + p.rk_b * rs.x, qv.y + p.rk_b * rs.y, qv.z + p.rk_b * rs.z, qv.w + p.rk_b * rs.w);
               } else {
-                if (p.accumulate) p.out[o] += r;
-                else p.out[o] = r;
+                if (p.accumulate) {
+                  const float4 o = *reinterpret_cast<const float4*>(outp + a + j);
+                  v.x += o.x;
+                  v.y += o.y;
+                  v.z += o.z;
+                  v.w += o.w;
+                }
+                *reinterpret_cast<float4*>(outp + a + j) = v;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (a + j >= Np) break;
+              if constexpr (OP == OP_STAGE) {
+                float x = resp[a + j] * p.rk_a;
+                x = x + p.dt * r[j];
+                resp[a + j] = x;
+                outp[a + j] = qp[a + j] + p.rk_b * x;
+              } else {
+                outp[a + j] = p.accumulate ? outp[a + j] + r[j] : r[j];
               }
             }
           }

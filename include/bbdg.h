@@ -140,6 +140,16 @@ int bbdg_step_host(bbdg_ctx* ctx, void* host_q, void* q, void* q_tmp, void* res,
                    const int64_t* bounds, int nchunks, int reach, void* stream, void* h2d_stream,
                    void* d2h_stream);
 
+/* bbdg_step_host for an ordinary (pageable) host state: the chunks move through
+ * context-owned pinned staging rings (allocated on first use, `slots` chunks per
+ * direction), filled and drained by `threads` host threads in parallel, so the
+ * host-side copies, both PCIe directions and the stages of other chunks overlap.
+ * Synchronous: host_q holds the new state on return.  Bitwise equal to
+ * bbdg_step.  Replaces the reference's lsrk4_step on a numpy q (solver.py:196-214). */
+int bbdg_step_pageable(bbdg_ctx* ctx, void* host_q, void* q, void* q_tmp, void* res, double dt, int lift_mode,
+                       const int64_t* bounds, int nchunks, int reach, int slots, int threads, void* stream,
+                       void* h2d_stream, void* d2h_stream);
+
 /* Pack the face traces of (elem, face) pairs (device int32 (n,2)) into
  * sendbuf (4, n, Nfp) in each face's own canonical order (halo send side). */
 int bbdg_halo_pack(bbdg_ctx* ctx, const void* q, void* sendbuf, const int32_t* faces, int64_t n, void* stream);

@@ -46,6 +46,8 @@ SIGNATURES = [
     ("bbdg_step", C.c_int, [_P, _P, _P, _P, _D, C.c_int, _P]),
     ("bbdg_step2", C.c_int, [_P, _P, _P, _P, _P, _D, C.c_int, _P]),
     ("bbdg_step_host", C.c_int, [_P, _P, _P, _P, _P, _D, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P]),
+    ("bbdg_step_pageable", C.c_int, [_P, _P, _P, _P, _P, _D, C.c_int, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P,
+                                     _P]),
     ("bbdg_halo_pack", C.c_int, [_P, _P, _P, _P, _I64, _P]),
     ("bbdg_energy", C.c_int, [C.c_int, _I64, C.c_int, _P, _P, _P, _P, _P, _P]),
     ("bbdg_error_l2", C.c_int, [C.c_int, _I64, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P]),

@@ -1,7 +1,10 @@
 // C ABI of libbbdg_cuda.so: context lifetime, table uploads, dispatch of the
 // tile kernels, the stand-alone LSRK update and the halo packer.
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -450,6 +453,7 @@ void bbdg_ctx_destroy(bbdg_ctx* c) {
   cudaFree(c->rhs_scratch);
   cudaFree(c->img_a);
   cudaFree(c->img_l);
+  cudaFreeHost(c->stage_ring);
   delete c;
 }
 
@@ -773,6 +777,194 @@ int bbdg_step_host(bbdg_ctx* c, void* host_q, void* q, void* q_tmp, void* res, d
   }
   for (auto e : ev)
     if (e) cudaEventDestroy(e);   // released once the queued work that uses it completes
+  return rc;
+}
+
+// Host copies of a pageable state through the pinned staging rings: the byte range of a job
+// list split evenly over `nthreads` threads (memcpy of one thread is ~10 GB/s, PCIe ~55).
+struct HostCopy {
+  char* dst;
+  const char* src;
+  size_t len;
+};
+static void parallel_copy(const std::vector<HostCopy>& jobs, int nthreads) {
+  size_t total = 0;
+  for (const HostCopy& j : jobs) total += j.len;
+  auto run = [&jobs](size_t b, size_t e) {
+    size_t pos = 0;
+    for (const HostCopy& j : jobs) {
+      const size_t js = pos, je = pos + j.len;
+      pos = je;
+      const size_t lo = b > js ? b : js, hi = e < je ? e : je;
+      if (lo < hi) std::memcpy(j.dst + (lo - js), j.src + (lo - js), hi - lo);
+    }
+  };
+  if (nthreads <= 1 || total < ((size_t)1 << 22)) {
+    run(0, total);
+    return;
+  }
+  const size_t per = ((total + nthreads - 1) / nthreads + 4095) & ~(size_t)4095;
+  std::vector<std::thread> pool;
+  for (int i = 1; i < nthreads && (size_t)i * per < total; ++i)
+    pool.emplace_back(run, (size_t)i * per, std::min(total, (size_t)(i + 1) * per));
+  run(0, std::min(total, per));
+  for (std::thread& t : pool) t.join();
+}
+
+int bbdg_step_pageable(bbdg_ctx* c, void* host_q, void* q, void* q_tmp, void* res, double dt, int lift,
+                       const int64_t* bounds, int nchunks, int reach, int slots, int threads, void* stream,
+                       void* h2d_stream, void* d2h_stream) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!host_q || !q || !q_tmp || !res || !bounds) return set_error(BBDG_ERR_ARG, "null pointer");
+  if (!(dt > 0.0)) return set_error(BBDG_ERR_ARG, "dt must be positive");
+  if (nchunks < 1 || reach < 0 || bounds[0] != 0 || bounds[nchunks] != c->K)
+    return set_error(BBDG_ERR_ARG, "chunk bounds must cover [0, K)");
+  if (slots < 1 || slots > 16 || threads < 1 || threads > 256) return set_error(BBDG_ERR_ARG, "bad slots / threads");
+  int64_t maxlen = 0;
+  for (int i = 0; i < nchunks; ++i) {
+    if (bounds[i + 1] <= bounds[i]) return set_error(BBDG_ERR_ARG, "chunk bounds must increase");
+    maxlen = std::max<int64_t>(maxlen, bounds[i + 1] - bounds[i]);
+  }
+  if (c->nhalo) return set_error(BBDG_ERR_ARG, "host-pipelined step on a partitioned context");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream), hs = static_cast<cudaStream_t>(h2d_stream),
+               ds = static_cast<cudaStream_t>(d2h_stream);
+  const size_t sz = c->dtype == BBDG_F32 ? 4 : 8, plane = (size_t)c->K * c->Np * sz;
+  const size_t slot_bytes = 4 * (size_t)maxlen * c->Np * sz, need = 2 * (size_t)slots * slot_bytes;
+  if (c->stage_ring_bytes < need) {
+    cudaFreeHost(c->stage_ring);
+    c->stage_ring = nullptr;
+    c->stage_ring_bytes = 0;
+    if (cudaError_t e = cudaHostAlloc(&c->stage_ring, need, cudaHostAllocDefault)) {
+      c->stage_ring = nullptr;
+      return set_cuda_error(e, "pinned staging ring");
+    }
+    c->stage_ring_bytes = need;
+  }
+  char* const in_ring = static_cast<char*>(c->stage_ring);
+  char* const out_ring = in_ring + (size_t)slots * slot_bytes;
+  char* const hq = static_cast<char*>(host_q);
+  auto chunk_off = [&](int i) { return (size_t)bounds[i] * c->Np * sz; };
+  auto chunk_len = [&](int i) { return (size_t)(bounds[i + 1] - bounds[i]) * c->Np * sz; };
+
+  std::vector<cudaEvent_t> ev(3 * nchunks + 1, nullptr);
+  int rc = BBDG_OK;
+  auto fail = [&](cudaError_t e, const char* where) {
+    if (rc == BBDG_OK) rc = set_cuda_error(e, where);
+    return rc;
+  };
+  for (auto& e : ev)
+    if (cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming)) {
+      fail(r, "event create");
+      break;
+    }
+  cudaEvent_t* h2d_done = ev.data();
+  cudaEvent_t* st5_done = ev.data() + nchunks;
+  cudaEvent_t* d2h_done = ev.data() + 2 * nchunks;
+  cudaEvent_t start = ev[3 * nchunks];
+  if (rc == BBDG_OK) {
+    if (cudaError_t r = cudaEventRecord(start, cs)) fail(r, "event record");
+    else if ((r = cudaStreamWaitEvent(hs, start, 0)) || (r = cudaStreamWaitEvent(ds, start, 0))) fail(r, "wait");
+  }
+  if (rc == BBDG_OK)
+    if (cudaError_t r = cudaMemsetAsync(res, 0, 4 * plane, cs)) fail(r, "res zeroing");
+
+  // drainer: waits for each chunk's D2H into its out slot, then copies the slot into host_q
+  std::mutex mu;
+  std::condition_variable cv;
+  int posted = 0, drained = 0;
+  bool stop = false;
+  std::thread drainer([&] {
+    for (int i = 0; i < nchunks; ++i) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return posted > i || stop; });
+        if (posted <= i) return;
+      }
+      cudaEventSynchronize(d2h_done[i]);
+      const size_t off = chunk_off(i), len = chunk_len(i);
+      const char* slot = out_ring + (size_t)(i % slots) * slot_bytes;
+      std::vector<HostCopy> jobs;
+      for (int F = 0; F < 4; ++F) jobs.push_back({hq + F * plane + off, slot + F * len, len});
+      parallel_copy(jobs, threads);
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        drained = i + 1;
+      }
+      cv.notify_all();
+    }
+  });
+
+  int fed = 0;
+  auto feed = [&](int i) {
+    const int sl = i % slots;
+    if (i >= slots)
+      if (cudaError_t r = cudaEventSynchronize(h2d_done[i - slots])) return fail(r, "staging slot wait");
+    const size_t off = chunk_off(i), len = chunk_len(i);
+    char* slot = in_ring + (size_t)sl * slot_bytes;
+    std::vector<HostCopy> jobs;
+    for (int F = 0; F < 4; ++F) jobs.push_back({slot + F * len, hq + F * plane + off, len});
+    parallel_copy(jobs, threads);
+    for (int F = 0; F < 4 && rc == BBDG_OK; ++F)
+      if (cudaError_t r = cudaMemcpyAsync(static_cast<char*>(q) + F * plane + off, slot + F * len, len,
+                                          cudaMemcpyHostToDevice, hs))
+        fail(r, "chunk copy");
+    if (rc == BBDG_OK)
+      if (cudaError_t r = cudaEventRecord(h2d_done[i], hs)) fail(r, "event record");
+    return rc;
+  };
+  void* buf[2] = {q, q_tmp};
+  const int lag = reach, nslot_t = nchunks + 4 * lag;
+  for (int t = 0; t < nslot_t && rc == BBDG_OK; ++t) {
+    for (int s = 0; s < 5 && rc == BBDG_OK; ++s) {
+      const int i = t - lag * s;
+      if (i < 0 || i >= nchunks) continue;
+      if (s == 0) {
+        const int need_i = i + reach < nchunks ? i + reach : nchunks - 1;
+        while (fed <= need_i && rc == BBDG_OK) feed(fed++);
+        if (rc != BBDG_OK) break;
+        if (cudaError_t r = cudaStreamWaitEvent(cs, h2d_done[need_i], 0)) {
+          fail(r, "wait");
+          break;
+        }
+      }
+      rc = bbdg_lsrk_stage_range(c, buf[s & 1], buf[(s + 1) & 1], res, lift, kRK4A[s], kRK4B[s], dt, bounds[i],
+                                 bounds[i + 1], stream);
+      if (rc == BBDG_OK && s == 4) {
+        cudaError_t r = cudaEventRecord(st5_done[i], cs);
+        if (!r) r = cudaStreamWaitEvent(ds, st5_done[i], 0);
+        if (r) {
+          fail(r, "event");
+          break;
+        }
+        if (i >= slots) {   // the out slot's previous chunk has been copied to host_q
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return drained >= i - slots + 1; });
+        }
+        const size_t off = chunk_off(i), len = chunk_len(i);
+        char* slot = out_ring + (size_t)(i % slots) * slot_bytes;
+        for (int F = 0; F < 4 && rc == BBDG_OK; ++F)
+          if ((r = cudaMemcpyAsync(slot + F * len, static_cast<const char*>(q_tmp) + F * plane + off, len,
+                                   cudaMemcpyDeviceToHost, ds)))
+            fail(r, "chunk copy");
+        if (rc == BBDG_OK && (r = cudaEventRecord(d2h_done[i], ds))) fail(r, "event record");
+        if (rc == BBDG_OK) {
+          std::lock_guard<std::mutex> lk(mu);
+          posted = i + 1;
+        }
+        cv.notify_all();
+      }
+    }
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    stop = true;
+  }
+  cv.notify_all();
+  drainer.join();
+  if (rc == BBDG_OK)
+    if (cudaError_t r = cudaStreamSynchronize(cs)) fail(r, "step");
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
   return rc;
 }
 

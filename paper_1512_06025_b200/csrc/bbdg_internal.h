@@ -28,6 +28,8 @@ struct bbdg_ctx {
   void* blift = nullptr;     // nodal blocked: L^T MMA fragments
   void* flux = nullptr;      // nodal blocked / BB dense on the tensor cores: (4, K, 4 Nfp) face-flux scratch
   void* rhs_scratch = nullptr;   // BB dense fused stage: (4, K, Np) rhs (allocated on first use)
+  void* stage_ring = nullptr;   // bbdg_step_pageable: pinned staging rings (cudaHostAlloc), in then out
+  size_t stage_ring_bytes = 0;
   void* img_a = nullptr;     // fp32 tcgen05 path: packed tf32 hi/lo image of q (bbdg_tc.cuh, first use)
   void* img_l = nullptr;     // fp32 tcgen05 path: packed tf32 hi/lo image of the face fluxes
   const void* halo = nullptr;

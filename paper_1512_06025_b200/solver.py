@@ -397,31 +397,32 @@ def host_chunk_plan(etoe, Np: int, itemsize: int, max_chunks: int = 48, min_stat
     return bounds, reach
 
 
+def _copy_threads() -> int:
+    n = os.environ.get("BBDG_COPY_THREADS")
+    return max(1, int(n)) if n else max(1, min(8, (os.cpu_count() or 2) // 2))
+
+
 def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -> bool:
-    """Pipelined H2D + five stages + D2H of a pinned host state (bbdg_step_host); False if not applicable."""
+    """Pipelined H2D + five stages + D2H of a host state; False if not applicable.
+
+    A pinned array (e.g. ``torch.empty(..., pin_memory=True).numpy()``) is copied directly by
+    ``bbdg_step_host``; an ordinary pageable array of at least 4 MB goes through the context's
+    pinned staging rings, filled and drained by host threads (``bbdg_step_pageable``), so that
+    the host copies, both PCIe directions and the stages of other chunks overlap.
+    """
     if system._plan is not None or system._box or not isinstance(q_host, np.ndarray) or not q_host.flags.c_contiguous \
             or not q_host.flags.writeable or q_host.dtype != np.dtype(system.dtype):
         return False
     torch = _torch()
-    registered = False
-    if not torch.from_numpy(q_host).is_pinned():
-        # an ordinary (pageable) numpy array: page-lock it for the duration of the step so the chunk
-        # copies are asynchronous and overlap the stages (pageable copies serialise with the kernels)
-        # (measured on the B200 boxes: page-locking costs ~5 GB/s, a win for states up to several hundred
-        # MB -- cube_mesh(40) N=5, 344 MB: 50 -> 26 ms per step -- and a loss above ~1 GB: N=9 194 -> 294 ms)
-        if not (32 << 20) <= q_host.nbytes <= (768 << 20) or os.environ.get("BBDG_HOST_REGISTER", "1") == "0":
-            return False
-        if int(torch._C._cudart.cudaHostRegister(q_host.ctypes.data, q_host.nbytes, 0)) != 0:
-            return False   # registration refused: the plain copy path
-        registered = True
+    pinned = torch.from_numpy(q_host).is_pinned()
+    if not pinned and q_host.nbytes < (4 << 20):
+        return False   # small: the plain copy path
     if not hasattr(system, "_chunks"):
         etoe = system.mesh.etoe
         if _is_tensor(etoe):
             etoe = etoe.cpu().numpy()
         system._chunks = host_chunk_plan(etoe, system.ops.Np, np.dtype(system.dtype).itemsize)
     if system._chunks is None:
-        if registered:
-            torch._C._cudart.cudaHostUnregister(q_host.ctypes.data)
         return False
     bounds, reach = system._chunks
     if not hasattr(system, "_copy_streams"):
@@ -430,13 +431,17 @@ def _host_step(system: "WaveSystem", q_host: np.ndarray, dt: float, lift: str) -
     q = system.empty_state()
     tmp, r = torch.empty_like(q), torch.empty_like(q)
     cs = torch.cuda.current_stream()
-    _lib.check(system._lib.bbdg_step_host(system._ctx, q_host.ctypes.data, q.data_ptr(), tmp.data_ptr(), r.data_ptr(),
-                                          float(dt), system._lift_id(lift), bounds.ctypes.data, len(bounds) - 1,
-                                          int(reach), cs.cuda_stream, hs.cuda_stream, ds.cuda_stream),
-               "bbdg_step_host")
-    cs.synchronize()   # host_q holds the new state (reference: in place on return)
-    if registered:
-        torch._C._cudart.cudaHostUnregister(q_host.ctypes.data)
+    if pinned:
+        _lib.check(system._lib.bbdg_step_host(system._ctx, q_host.ctypes.data, q.data_ptr(), tmp.data_ptr(),
+                                              r.data_ptr(), float(dt), system._lift_id(lift), bounds.ctypes.data,
+                                              len(bounds) - 1, int(reach), cs.cuda_stream, hs.cuda_stream,
+                                              ds.cuda_stream), "bbdg_step_host")
+        cs.synchronize()   # host_q holds the new state (reference: in place on return)
+    else:
+        _lib.check(system._lib.bbdg_step_pageable(system._ctx, q_host.ctypes.data, q.data_ptr(), tmp.data_ptr(),
+                                                  r.data_ptr(), float(dt), system._lift_id(lift), bounds.ctypes.data,
+                                                  len(bounds) - 1, int(reach), 3, _copy_threads(), cs.cuda_stream,
+                                                  hs.cuda_stream, ds.cuda_stream), "bbdg_step_pageable")
     return True
 
 
@@ -455,7 +460,7 @@ def lsrk4_step(system, state: FieldState, dt: float, lift_mode: str = "factorize
         system._check(state)
         lift = system._nodal_mode(lift_mode)
         system._lift_id(lift)
-        # pinned numpy state, fresh res: copies in both directions overlap the stages chunk by chunk
+        # numpy state, fresh res: copies in both directions overlap the stages chunk by chunk
         if res is None and _host_step(system, state.q, dt, lift):
             return FieldState(state.q, state.basis, t0 + dt)
         q = system.to_device(state.q)

@@ -99,13 +99,55 @@ def test_pipelined_step_bitwise_equals_device_step(N, dname, halve):
 
 
 @pytest.mark.gpu
-def test_pageable_state_uses_plain_path_and_matches():
+@pytest.mark.parametrize("N,dname,halve,threads", [(4, "f32", False, 1), (4, "f32", True, 4), (7, "f64", True, 3)])
+def test_pageable_state_staged_pipeline_bitwise(N, dname, halve, threads, monkeypatch):
+    """An ordinary numpy state goes through the pinned staging rings (bbdg_step_pageable): more
+    chunks than ring slots, several copy threads, bitwise equal to the device-tensor step."""
     import torch
 
+    monkeypatch.setenv("BBDG_COPY_THREADS", str(threads))
+    dtype = np.float64 if dname == "f64" else np.float32
     m = cube_mesh(12)
+    sy = WaveSystem(m, BernsteinRefOps.build(N), Materials.homogeneous(m.K), dtype=dtype)
+    band = int(np.abs(m.etoe - np.arange(m.K)[:, None]).max())
+    sy._chunks = host_chunk_plan(m.etoe, sy.Np, np.dtype(dtype).itemsize, min_state_bytes=0,
+                                 chunk=(band // 2 + 1) if halve else None)
+    assert len(sy._chunks[0]) - 1 > 3              # more chunks than the 3 ring slots
+    q0 = np.random.default_rng(3).standard_normal((4, m.K, sy.Np)).astype(dtype)
+    assert q0.nbytes >= 4 << 20
+    dt = stable_dt(m, N, 1.0)
+    calls = []
+    lib = sy._lib
+
+    class Spy:
+        def __getattr__(self, k):
+            if k == "bbdg_step_pageable":
+                calls.append(1)
+            return getattr(lib, k)
+
+    sy._lib = Spy()
+    a = FieldState(q0.copy(), "bernstein")
+    try:
+        for _ in range(2):
+            a = lsrk4_step(sy, a, dt, "optimal")
+    finally:
+        sy._lib = lib
+    b = FieldState(torch.from_numpy(q0.copy()).cuda(), "bernstein")
+    for _ in range(2):
+        b = lsrk4_step(sy, b, dt, "optimal")
+    assert len(calls) == 2
+    assert np.array_equal(a.q, b.q.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_small_pageable_state_uses_plain_path_and_matches():
+    import torch
+
+    m = cube_mesh(6)
     sy = WaveSystem(m, BernsteinRefOps.build(4), Materials.homogeneous(m.K), dtype=np.float32)
     sy._chunks = host_chunk_plan(m.etoe, sy.Np, 4, min_state_bytes=0)
     q0 = np.random.default_rng(3).standard_normal((4, m.K, sy.Np)).astype(np.float32)
+    assert q0.nbytes < 4 << 20
     dt = stable_dt(m, 4, 1.0)
     a = lsrk4_step(sy, FieldState(q0.copy(), "bernstein"), dt, "optimal")       # pageable numpy
     b = lsrk4_step(sy, FieldState(torch.from_numpy(q0.copy()).cuda(), "bernstein"), dt, "optimal")

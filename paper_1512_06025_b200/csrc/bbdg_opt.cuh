@@ -68,7 +68,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ----------------------------------------------------------------------------
 // (tuning builds may override the tables: -DBBDG_OPT_KE4=0,32,... etc.)
 #ifndef BBDG_OPT_KE4
-#define BBDG_OPT_KE4 0, 32, 16, 12, 6, 4, 3, 2, 2, 1   // (N=2: KE 16 -> 4 groups, +5.6 %)
+#define BBDG_OPT_KE4 0, 32, 16, 12, 6, 4, 3, 3, 2, 1   // (N=2: KE 16 -> 4 groups, +5.6 %; N=7: KE 3, +4 % with 4 groups)
 #endif
 #ifndef BBDG_OPT_KE8
 #define BBDG_OPT_KE8 0, 16, 12, 6, 4, 2, 2, 2, 1, 1   // (N=6: KE 2 -> 4 groups, +7 % with res from HBM)
@@ -110,6 +110,11 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_shf_slots() {
 #ifndef BBDG_OPT_NG_TMEM
 #define BBDG_OPT_NG_TMEM 5   // groups of the fused fp32 kernels whose hoisted tables live in TMEM
 #endif
+#ifndef BBDG_OPT_NGT4
+// per order (fp32 fused stage / rhs in TMEM mode); measured on the HBM-filling boxes (same box,
+// interleaved A/B): 4 groups at N = 6, 7 +5.3 % / +4.0 % (with KE 3 at N = 7), other orders neutral or worse
+#define BBDG_OPT_NGT4 0, 5, 5, 5, 5, 5, 4, 4, 5, 5
+#endif
 // per order: the stage reads the LSRK register straight from HBM in the epilogue instead of
 // staging it (frees shared memory for more groups where shared memory caps them)
 #ifndef BBDG_OPT_RESG4
@@ -141,7 +146,8 @@ template <int N, int SZ, int OP> __host__ __device__ constexpr int opt_max_group
   if constexpr (OP == 0) return BBDG_OPT_NG_VOL;   // OP_VOLUME
   if constexpr (OP == 1) return (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) ? BBDG_OPT_NG_TMEM
                                                                                      : BBDG_OPT_NG_SURF;  // OP_SURFACE
-  if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return BBDG_OPT_NG_TMEM;
+  constexpr int gt4[10] = {BBDG_OPT_NGT4};
+  if constexpr (BBDG_OPT_TMEM && SZ == 4 && N >= BBDG_OPT_TMEM_MIN_N) return gt4[N];
   constexpr int gt8[10] = {BBDG_OPT_NGT8};
   if constexpr (BBDG_OPT_TMEM && BBDG_OPT_TMEM64 && SZ == 8 && N >= BBDG_OPT_TMEM64_MIN_N) return gt8[N];
   return SZ == 4 ? g4[N] : g8[N];

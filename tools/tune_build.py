@@ -9,6 +9,13 @@ F64 = set()
 VARIANTS = {
     "k2": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,2,2,1"],   # fp32 N=2: KE 16
     "k3": ["-DBBDG_OPT_KE4=0,32,24,8,6,4,3,2,2,1"],    # fp32 N=3: KE 8
+    "keup": ["-DBBDG_OPT_KE4=0,32,16,12,6,5,4,3,3,2"],   # fp32 N >= 5: one more element per tile
+    "kedn": ["-DBBDG_OPT_KE4=0,32,16,12,6,3,2,2,1,1"],   # fp32 N >= 5: one fewer
+    "ng4": ["-DBBDG_OPT_NG_TMEM=4"],                     # TMEM-mode groups per CTA
+    "ng6": ["-DBBDG_OPT_NG_TMEM=6"],
+    "v1": ["-DBBDG_OPT_NGT4=0,5,5,5,5,5,4,4,5,5", "-DBBDG_OPT_KE4=0,32,16,12,6,4,3,3,2,1"],
+    "v2": ["-DBBDG_OPT_NGT4=0,5,5,5,5,5,4,4,5,5"],
+    "v3": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,3,2,1"],
 }
 
 if __name__ == "__main__":

@@ -3,23 +3,25 @@
 // SURVEY K6/K7; reference nodal.py:220-241 through WaveSystem, solver.py:139-190).  fp64 keeps
 // the DMMA kernel of bbdg_nodal.cuh (tcgen05 has no f64 kind).
 //
-// A CTA tile is 32 elements x 4 fields = 128 GEMM rows (row 4e + F: the four fields of an element
-// sit in adjacent TMEM lanes of one warp).  Per block of NB output nodes:
+// A 128-row sub-tile is 32 elements x 4 fields (row 4e + F: the four fields of an element sit in
+// adjacent TMEM lanes of one warp).  Per block of NB output nodes:
 //   volume  C_v[row][(m, a)] = sum_b Q[row][b] D_m[a][b]      (N = 3 NB, K = Np)
 //   lift    C_l[row][a]      = sum_c X[row][c] L[a][c]        (N = NB,   K = 4 Nfp)
-// with X = (Fp, n1 Fu, n2 Fu, n3 Fu) from nodal_flux_kernel.  fp32 accuracy from 3xTF32: every
-// k-step issues lo*hi + hi*lo + hi*hi (x = hi + lo split at tf32 precision, cvt.rna), so the
-// products carry ~fp32 precision (TF32 alone: ~5e-4, SURVEY 7 "hard part 5").
+// with X = (Fp, n1 Fu, n2 Fu, n3 Fu), the face fluxes.  fp32 accuracy from 3xTF32: every k-step
+// issues lo*hi + hi*lo + hi*hi (x = hi + lo split at tf32 precision, cvt.rna), so the products
+// carry ~fp32 precision (TF32 alone: ~5e-4, SURVEY 7 "hard part 5").
 //
-// Operands stream through two shared-memory stages in the canonical no-swizzle K-major UMMA
-// layout (8-row x 16-byte core matrices; LBO = 128 B between K-adjacent core matrices, SBO =
-// KC/4 x 128 B between row groups).  The operator chunks are pre-arranged on the host in exactly
-// that image (hi and lo), so they are plain 16-byte copies; the element tiles are split into
-// hi / lo while being stored.  One elected thread issues the MMAs and commits them to an
-// mbarrier per stage, so the loads of chunk c+1 overlap the MMAs of chunk c.  The epilogue reads
-// the accumulators with tcgen05.ld (lane = row), combines the 3 derivative columns of the four
-// field lanes of an element with warp shuffles (chain rule, solver.py:148-157), adds the material-
-// scaled lift (solver.py:182-189) and writes the rhs or the LSRK stage (solver.py:211-213).
+// All operands are tf32 hi / lo images in the canonical no-swizzle K-major UMMA layout (8-row x
+// 16-byte core matrices; LBO = 128 B between K-adjacent core matrices, SBO = KC/4 x 128 B between
+// row groups): the operator chunks built once on the host (tc_operator_images), the element rows
+// by tc_pack_kernel (q) and tc_flux_kernel (fluxes computed straight into the image) before the
+// GEMM.  nodal_tc_kernel is warp-specialised: a producer warp streams (element chunk, operator
+// chunk) pairs into NS stages with cp.async.bulk, one thread of the MMA warp issues the MMAs and
+// commits each stage back to the producer and each finished node block to the epilogue, and four
+// epilogue warps read the double-buffered accumulators with tcgen05.ld (lane = row), combine the
+// 3 derivative columns of the element's four field lanes with shuffles (chain rule,
+// solver.py:148-157), add the material-scaled lift (solver.py:182-189) and write the rhs or the
+// LSRK stage (solver.py:211-213).
 #pragma once
 #include <vector>
 
@@ -76,8 +78,7 @@ template <int N> struct TcLayout {
   static constexpr int TM_COLS = 2 * ABUF <= 128 ? 128 : (2 * ABUF <= 256 ? 256 : 512);
   static_assert(2 * ABUF <= 512, "accumulators exceed the TMEM columns");
   static_assert(NS >= 2 && total <= 227 * 1024, "tcgen05 nodal tile does not fit in shared memory");
-  // packed element image: [step][kc][sub-tile][hi, lo][UMMA rows x KC]
-  static int64_t img_floats(int64_t nl, int nk) { return ((nl + ST - 1) / ST) * nk * (ABLK / 4); }
+  // packed element image: [step][kc][sub-tile][hi, lo][UMMA rows x KC] (tc_image_bytes)
 };
 
 // byte offset of element (row, k) (k in the chunk) in the canonical no-swizzle K-major layout

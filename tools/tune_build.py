@@ -5,7 +5,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"e8", "f8"}
+F64 = {"e8", "f8", "ept64"}
 VARIANTS = {
     "k2": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,2,2,1"],   # fp32 N=2: KE 16
     "k3": ["-DBBDG_OPT_KE4=0,32,24,8,6,4,3,2,2,1"],    # fp32 N=3: KE 8
@@ -19,6 +19,8 @@ VARIANTS = {
     "d4": ["-DBBDG_OPT_NGT4=0,5,5,5,6,6,4,4,4,4"],            # fp32 N=4,5: 6 groups, N=8,9: 4
     "e8": ["-DBBDG_OPT_KE8=0,16,12,6,5,3,3,3,2,2"],           # fp64 N >= 4: one more element per tile
     "f8": ["-DBBDG_OPT_NGT8=0,4,4,5,5,5,5,5,5,5"],            # fp64 TMEM-mode groups 5 at N >= 4
+    "ept64": ["-DBBDG_EPT_MAX_N64=3"],                         # fp64 N=3 on the register kernel
+    "ept4": ["-DBBDG_EPT_MAX_N=4"],                            # fp32 N=4 on the register kernel
 }
 
 if __name__ == "__main__":

@@ -766,8 +766,14 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
             fstride = p.nhalo * Nfp;
           }
           const uint32_t d = sn + hi16(s_of[k]) * sz;
+#ifndef BBDG_EXP_NO_NB   // (experiment only: skip the neighbour-trace gather to bound its cost)
 #pragma unroll
           for (int F = 0; F < 4; ++F) cp_async<sz>(d + F * NB * sz, src + F * fstride);
+#else
+          (void)d;
+          (void)src;
+          (void)fstride;
+#endif
         }
       });
     });

@@ -21,6 +21,7 @@ VARIANTS = {
     "f8": ["-DBBDG_OPT_NGT8=0,4,4,5,5,5,5,5,5,5"],            # fp64 TMEM-mode groups 5 at N >= 4
     "ept64": ["-DBBDG_EPT_MAX_N64=3"],                         # fp64 N=3 on the register kernel
     "ept4": ["-DBBDG_EPT_MAX_N=4"],                            # fp32 N=4 on the register kernel
+    "nonb": ["-DBBDG_EXP_NO_NB=1"],                              # experiment: no neighbour gather (wrong results)
 }
 
 if __name__ == "__main__":

@@ -123,6 +123,21 @@ template <int N, int SZ> __host__ __device__ constexpr int opt_shf_slots() {
 #ifndef BBDG_OPT_RESG8
 #define BBDG_OPT_RESG8 0, 0, 0, 1, 1, 1, 1, 1, 1, 1   // (measured: N = 1, 2 lose 3-9 %; not smem-bound)
 #endif
+// per order: faces whose neighbour lies inside the tile (and boundary faces) read the neighbour
+// trace from the staged state instead of gathering it (measured A/B on the HBM-filling boxes,
+// fp32: N=5 +2.5 %, N=8 +8.7 %, N=4, 6, 7, 9 lose 2-6 % to the divergent S1 path; fp64: N=3
+// +8.6 %, N=6 +1.2 %, the others lose up to 2.6 %)
+#ifndef BBDG_OPT_LOCNB4
+#define BBDG_OPT_LOCNB4 0, 0, 0, 0, 0, 1, 0, 0, 1, 0
+#endif
+#ifndef BBDG_OPT_LOCNB8
+#define BBDG_OPT_LOCNB8 0, 0, 0, 1, 0, 0, 1, 0, 0, 0
+#endif
+template <int N, int SZ> __host__ __device__ constexpr bool opt_local_nb() {
+  constexpr int l4[10] = {BBDG_OPT_LOCNB4};
+  constexpr int l8[10] = {BBDG_OPT_LOCNB8};
+  return (SZ == 4 ? l4[N] : l8[N]) != 0;
+}
 template <int N, int SZ> __host__ __device__ constexpr bool opt_res_global() {
   constexpr int r4[10] = {BBDG_OPT_RESG4};
   constexpr int r8[10] = {BBDG_OPT_RESG8};
@@ -212,7 +227,11 @@ template <typename T, int N, int OP, int FSR> struct OptLayout {
   static constexpr int t_res = rnd(t_q + 4 * S + 2 * A);          // same shape (RES)
   static constexpr int t_geo = rnd(t_res + (RESS ? 4 * S + 2 * A : 0));   // [KE][36]
   static constexpr int t_nb = rnd(t_geo + KE * kGeoRec);          // [4][NB]
-  static constexpr int t_bar = rnd(t_nb + (SURF ? 4 * NB : 0));   // mbarrier (8 bytes)
+  // per face of the tile: neighbour inside the tile ((k2 - k0) << 16 | trace key; read from the
+  // staged state instead of gathered) or ~0 (gathered into t_nb)
+  static constexpr bool LOCNB = SURF && opt_local_nb<N, sz>();
+  static constexpr int t_loc = rnd(t_nb + (SURF ? 4 * NB : 0));
+  static constexpr int t_bar = rnd(t_loc + (LOCNB ? (16 * KE + sz - 1) / sz : 0));   // mbarrier (8 bytes)
   static constexpr int stage_T = rnd(t_bar + 8 / sz + 1);
   static constexpr int RQ = t_res - t_q;                          // res distance from q (elements)
   // group block (units of T)
@@ -747,10 +766,12 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
   };
   auto issue_nb = [&](int64_t k0, int nv, int st) {
     const uint32_t sn = smem_u32(stage_ptr(st) + L::t_nb);
+    uint32_t* sloc = reinterpret_cast<uint32_t*>(stage_ptr(st) + L::t_loc);
     static_for<0, SS>([&](auto KK) {
       constexpr int k = decltype(KK)::value;
       slot<k, 32, NSI>(lane, [&] {
         const int m = s_ef[k] & 0xff, f = (s_ef[k] >> 8) & 3, e = s_ef[k] >> 10;
+        uint32_t loc = ~0u;
         if (e < nv) {
           const int cd = (ncode[k] >> (8 * f)) & 0xff;
           const bool bnd = cd & 32;
@@ -760,21 +781,28 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
             // interior: neighbour's trace; boundary: own trace (the mirror sign lives in Bs)
             const int key = bnd ? f * 6 : (cd & 3) * 6 + ((cd >> 2) & 7);
             const int64_t k2 = bnd ? k0 + e : (int64_t)nnbr[k];
+            // a neighbour inside the tile (a third of the faces at KE = 3, half at KE = 6, every
+            // boundary face) is read from the staged state in S1: no gather
+            if (L::LOCNB && k2 >= k0 && k2 < k0 + nv) loc = ((uint32_t)(k2 - k0) << 16) | (uint32_t)key;
             src = q + k2 * Np + tr2[key * Nfp + m];
           } else {
             src = p.halo + (int64_t)nnbr[k] * Nfp + ptab[((cd >> 2) & 7) * Nfp + m];
             fstride = p.nhalo * Nfp;
           }
+          if (loc != ~0u) src = nullptr;
           const uint32_t d = sn + hi16(s_of[k]) * sz;
 #ifndef BBDG_EXP_NO_NB   // (experiment only: skip the neighbour-trace gather to bound its cost)
+          if (src) {
 #pragma unroll
-          for (int F = 0; F < 4; ++F) cp_async<sz>(d + F * NB * sz, src + F * fstride);
+            for (int F = 0; F < 4; ++F) cp_async<sz>(d + F * NB * sz, src + F * fstride);
+          }
 #else
           (void)d;
           (void)src;
           (void)fstride;
 #endif
         }
+        if (L::LOCNB && m == 0) sloc[(s_ef[k] >> 8)] = loc;   // one entry per face (ef = 4 e + f)
       });
     });
   };
@@ -810,6 +838,7 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
     const T* sq = stg + L::t_q + (int)((k0 * Np) % A);   // field F at sq + F S; res at sq + RQ + F S
     const T* sgeo = stg + L::t_geo;
     const T* snb = stg + L::t_nb;
+    const uint32_t* sloc = reinterpret_cast<const uint32_t*>(stg + L::t_loc);
     mbar_wait(stage_bar(st), (it >> 1) & 1);
 
     // ------------------------------------------------------------- S1: upwind flux (solver.py:166-184)
@@ -823,10 +852,21 @@ __global__ void __launch_bounds__(OptLayout<T, N, OP, FSR>::threads, 1) opt_kern
           const V4<T> nf = *reinterpret_cast<const V4<T>*>(gr + 4 * f);
           const T tp = gr[16 + 2 * f], cu = gr[17 + 2 * f];
           T loc[4], nb[4];
+          // neighbour trace: staged state (neighbour inside the tile, or own trace on a boundary)
+          // or the gathered buffer
+          const T* nbp = snb + fl;
+          int nbs = NB;
+          if constexpr (L::LOCNB) {
+            const uint32_t lc = sloc[s_ef[k] >> 8];
+            if (lc != ~0u) {
+              nbp = sq + (int)(lc >> 16) * Np + tr2[(lc & 0xffff) * Nfp + (s_ef[k] & 0xff)];
+              nbs = S;
+            }
+          }
 #pragma unroll
           for (int F = 0; F < 4; ++F) {
             loc[F] = sq[F * S + own];
-            nb[F] = snb[F * NB + fl];
+            nb[F] = nbp[F * nbs];
           }
           const T bs = nf.w, ab = fabs(bs);
           const T u = bs * nb[0] - ab * loc[0];   // |Bs| jp

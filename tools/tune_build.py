@@ -5,7 +5,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"e8", "f8", "ept64"}
+F64 = {"e8", "f8", "ept64", "loc64"}
 VARIANTS = {
     "k2": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,2,2,1"],   # fp32 N=2: KE 16
     "k3": ["-DBBDG_OPT_KE4=0,32,24,8,6,4,3,2,2,1"],    # fp32 N=3: KE 8
@@ -21,7 +21,8 @@ VARIANTS = {
     "f8": ["-DBBDG_OPT_NGT8=0,4,4,5,5,5,5,5,5,5"],            # fp64 TMEM-mode groups 5 at N >= 4
     "ept64": ["-DBBDG_EPT_MAX_N64=3"],                         # fp64 N=3 on the register kernel
     "ept4": ["-DBBDG_EPT_MAX_N=4"],                            # fp32 N=4 on the register kernel
-    "nonb": ["-DBBDG_EXP_NO_NB=1"],                              # experiment: no neighbour gather (wrong results)
+    "nonb": ["-DBBDG_EXP_NO_NB=1"],
+    "loc64": ["-DBBDG_OPT_LOCNB8=0,0,0,1,1,1,1,1,1,1"],        # fp64: in-tile neighbour traces at N >= 3                              # experiment: no neighbour gather (wrong results)
 }
 
 if __name__ == "__main__":

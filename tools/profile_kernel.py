@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--n", type=int, default=26)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--box", default=None, help="nx,ny,nz: a device-built BoxMesh (e.g. the bench's fill mesh)")
+    ap.add_argument("--xblock", type=int, default=1, help="element order of the box (x-layers per slab)")
     a = ap.parse_args()
     import torch
 
@@ -34,7 +35,7 @@ def main():
     if a.box:
         from paper_1512_06025_b200.mesh_device import BoxMesh
 
-        m = BoxMesh(*[int(x) for x in a.box.split(",")])
+        m = BoxMesh(*[int(x) for x in a.box.split(",")], xblock=a.xblock)
         sy = WaveSystem(m, ops, Materials(np.float64(1.0), np.float64(1.0)), dtype=dt, legacy_records=False)
     else:
         m = cube_mesh(a.n)

@@ -115,19 +115,56 @@ template <typename T, int N> struct NodalLayout {
   static constexpr int total = (sf + 4 * ET * LF) * (int)sizeof(T);
 };
 
+// Face-point position tables of the nodal flux kernels, built per CTA in shared memory:
+//   own[f Nfp + m]            node of face f's point m (own canonical order)
+//   nbt[(f2 6 + s) Nfp + m]   node of the neighbour's face f2 matching point m under vertex
+//                             permutation s (multiindex.PERMS3)
+//   hpt[s Nfp + m]            point index in a halo face's canonical order under permutation s
+template <int N> struct FluxTab {
+  static constexpr int Nfp = Dims<N>::Nfp;
+  static constexpr int own = 0, nbt = 4 * Nfp, hpt = 28 * Nfp, total = 34 * Nfp;   // uint16 entries
+};
+template <int N> __device__ void build_flux_tables(uint16_t* t) {
+  using TB = FluxTab<N>;
+  constexpr int Nfp = TB::Nfp;
+  const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  for (int i = threadIdx.x; i < TB::total; i += blockDim.x) {
+    const int r = i < TB::nbt ? i : (i < TB::hpt ? i - TB::nbt : i - TB::hpt);
+    const int key = r / Nfp, m = r - key * Nfp;
+    int b0, b1;
+    decode2(N, m, b0, b1);
+    const int b[3] = {b0, b1, N - b0 - b1};
+    int v;
+    if (i < TB::nbt) {   // own: face key, point m
+      int a[4], s = 0;
+      for (int x = 0; x < 4; ++x) a[x] = (x == key) ? 0 : b[s++];
+      v = pos3(N, a[0], a[1], a[2]);
+    } else {
+      const int f2 = i < TB::hpt ? key / 6 : 0, sp = i < TB::hpt ? key % 6 : key;
+      int c[3];
+      for (int kk = 0; kk < 3; ++kk) c[perms[sp][kk]] = b[kk];
+      if (i < TB::hpt) {
+        int a2[4], s3 = 0;
+        for (int x = 0; x < 4; ++x) a2[x] = (x == f2) ? 0 : c[s3++];
+        v = pos3(N, a2[0], a2[1], a2[2]);
+      } else {
+        v = pos2(N, c[0], c[1]);
+      }
+    }
+    t[i] = (uint16_t)v;
+  }
+  __syncthreads();
+}
+
 // Face flux of the nodal path at face point fm = f Nfp + m of element k:
-// fl = (Fp, n1 Fu, n2 Fu, n3 Fu)   (solver.py:166-185)
+// fl = (Fp, n1 Fu, n2 Fu, n3 Fu)   (solver.py:166-185); tab from build_flux_tables
 template <typename T, int N>
-__device__ __forceinline__ void nodal_face_flux(const Params<T>& p, int64_t k, int fm, T fl[4]) {
-  constexpr int Np = Dims<N>::Np, Nfp = Dims<N>::Nfp;
+__device__ __forceinline__ void nodal_face_flux(const Params<T>& p, const uint16_t* tab, int64_t k, int fm, T fl[4]) {
+  using TB = FluxTab<N>;
+  constexpr int Np = Dims<N>::Np, Nfp = TB::Nfp;
   const int64_t fs = p.K * Np;
   const int f = fm / Nfp, m = fm - f * Nfp;
-  int b0, b1;
-  decode2(N, m, b0, b1);
-  const int b[3] = {b0, b1, N - b0 - b1};
-  int a[4], s = 0;
-  for (int v = 0; v < 4; ++v) a[v] = (v == f) ? 0 : b[s++];
-  const int pos = pos3(N, a[0], a[1], a[2]);
+  const int pos = tab[TB::own + fm];
   const T* gs = p.geo_surf + k * kGeoSurf + f * 6;
   const int cd = (p.code[k] >> (8 * f)) & 0xff;
   const bool bnd = (cd >> 5) & 1;
@@ -138,20 +175,14 @@ __device__ __forceinline__ void nodal_face_flux(const Params<T>& p, int64_t k, i
 #pragma unroll
     for (int F = 0; F < 4; ++F) nb[F] = loc[F];
   } else {
-    // neighbour point: the shared face's vertex permutation (multiindex.PERMS3)
-    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
     const int s2 = (cd >> 2) & 7, f2 = cd & 3;
-    int c[3];
-    for (int kk = 0; kk < 3; ++kk) c[perms[s2][kk]] = b[kk];
-    const int m2 = pos2(N, c[0], c[1]);
     const int64_t k2 = p.nbr[k * 4 + f];
     if ((cd >> 6) & 1) {
+      const int m2 = tab[TB::hpt + s2 * Nfp + m];
 #pragma unroll
       for (int F = 0; F < 4; ++F) nb[F] = p.halo[(F * p.nhalo + k2) * Nfp + m2];
     } else {
-      int a2[4], s3 = 0;
-      for (int v = 0; v < 4; ++v) a2[v] = (v == f2) ? 0 : c[s3++];
-      const int pos2n = pos3(N, a2[0], a2[1], a2[2]);
+      const int pos2n = tab[TB::nbt + (f2 * 6 + s2) * Nfp + m];
 #pragma unroll
       for (int F = 0; F < 4; ++F) nb[F] = p.q[F * fs + k2 * Np + pos2n];
     }
@@ -173,11 +204,13 @@ __global__ void __launch_bounds__(256) nodal_flux_kernel(const Params<T> p) {
   constexpr int Nfp = Dims<N>::Nfp;
   const int64_t nl = p.kend - p.kbeg;
   const int64_t total = nl * 4 * Nfp;
+  __shared__ uint16_t tab[FluxTab<N>::total];
+  build_flux_tables<N>(tab);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = x / (4 * Nfp);
     const int fm = (int)(x - e * 4 * Nfp);
     T fl[4];
-    nodal_face_flux<T, N>(p, p.kbeg + e, fm, fl);
+    nodal_face_flux<T, N>(p, tab, p.kbeg + e, fm, fl);
     T* o = p.flux + e * 4 * Nfp + fm;
     const int64_t ps = nl * 4 * Nfp;
 #pragma unroll

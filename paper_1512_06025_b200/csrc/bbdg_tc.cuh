@@ -169,11 +169,13 @@ __global__ void __launch_bounds__(256) tc_flux_kernel(const Params<float> p) {
   const int64_t nl = p.kend - p.kbeg;
   const int64_t total = nl * 4 * Nfp;
   unsigned char* img = static_cast<unsigned char*>(p.img_l);
+  __shared__ uint16_t tab[FluxTab<N>::total];
+  build_flux_tables<N>(tab);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = x / (4 * Nfp);
     const int fm = (int)(x - e * 4 * Nfp);
     float fl[4];
-    nodal_face_flux<float, N>(p, p.kbeg + e, fm, fl);
+    nodal_face_flux<float, N>(p, tab, p.kbeg + e, fm, fl);
     const int64_t step = e / L::ST;
     const int el = (int)(e - step * L::ST), t = el / L::KE, kc = fm / L::KC;
     unsigned char* blk = img + (step * L::KL + kc) * (int64_t)L::ABLK + t * 2 * L::A_BYTES;

@@ -5,7 +5,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1512_06025_b200.build import build_variant  # noqa: E402
 
-F64 = {"e8", "f8", "ept64", "loc64"}
+F64 = {"e8", "f8", "ept64", "loc64", "nonb64"}
+BOTH = {"eptold"}
 VARIANTS = {
     "k2": ["-DBBDG_OPT_KE4=0,32,16,12,6,4,3,2,2,1"],   # fp32 N=2: KE 16
     "k3": ["-DBBDG_OPT_KE4=0,32,24,8,6,4,3,2,2,1"],    # fp32 N=3: KE 8
@@ -22,6 +23,8 @@ VARIANTS = {
     "ept64": ["-DBBDG_EPT_MAX_N64=3"],                         # fp64 N=3 on the register kernel
     "ept4": ["-DBBDG_EPT_MAX_N=4"],                            # fp32 N=4 on the register kernel
     "nonb": ["-DBBDG_EXP_NO_NB=1"],
+    "nonb64": ["-DBBDG_EXP_NO_NB=1"],
+    "eptold": ["-DBBDG_EPT_LOCNB=0"],                          # EPT without the in-tile neighbour copies
     "loc64": ["-DBBDG_OPT_LOCNB8=0,0,0,1,1,1,1,1,1,1"],        # fp64: in-tile neighbour traces at N >= 3                              # experiment: no neighbour gather (wrong results)
 }
 
@@ -32,4 +35,4 @@ if __name__ == "__main__":
         d.mkdir(parents=True, exist_ok=True)
         hdr = d / "tune.h"
         hdr.write_text("".join(f"#define {x[2:].split('=')[0]} {x.split('=', 1)[1]}\n" for x in VARIANTS[n]))
-        print(n, build_variant(d, ["--pre-include", str(hdr)], dtypes=("f64",) if n in F64 else ("f32",)))
+        print(n, build_variant(d, ["--pre-include", str(hdr)], dtypes=("f32", "f64") if n in BOTH else (("f64",) if n in F64 else ("f32",))))

@@ -805,9 +805,16 @@ static void parallel_copy(const std::vector<HostCopy>& jobs, int nthreads) {
   }
   const size_t per = ((total + nthreads - 1) / nthreads + 4095) & ~(size_t)4095;
   std::vector<std::thread> pool;
-  for (int i = 1; i < nthreads && (size_t)i * per < total; ++i)
-    pool.emplace_back(run, (size_t)i * per, std::min(total, (size_t)(i + 1) * per));
+  size_t done = per;   // [0, done) is this thread's; ranges whose thread could not start run here too
+  try {
+    for (int i = 1; i < nthreads && (size_t)i * per < total; ++i) {
+      pool.emplace_back(run, (size_t)i * per, std::min(total, (size_t)(i + 1) * per));
+      done = std::min(total, (size_t)(i + 1) * per);
+    }
+  } catch (...) {   // no more threads (std::system_error): copy the rest on this one
+  }
   run(0, std::min(total, per));
+  if (done < total) run(done, total);
   for (std::thread& t : pool) t.join();
 }
 
@@ -873,7 +880,7 @@ int bbdg_step_pageable(bbdg_ctx* c, void* host_q, void* q, void* q_tmp, void* re
   std::condition_variable cv;
   int posted = 0, drained = 0;
   bool stop = false;
-  std::thread drainer([&] {
+  auto drain = [&] {
     for (int i = 0; i < nchunks; ++i) {
       {
         std::unique_lock<std::mutex> lk(mu);
@@ -892,7 +899,15 @@ int bbdg_step_pageable(bbdg_ctx* c, void* host_q, void* q, void* q_tmp, void* re
       }
       cv.notify_all();
     }
-  });
+  };
+  std::thread drainer;
+  try {
+    drainer = std::thread(drain);
+  } catch (...) {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    return set_error(BBDG_ERR_CUDA, "could not start the staging drainer thread");
+  }
 
   int fed = 0;
   auto feed = [&](int i) {

@@ -43,7 +43,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1)
     q = torch.randn((4, m.K, sy.Np), dtype=sy.torch_dtype, device="cuda", generator=g)
     q2, res = torch.empty_like(q), torch.randn_like(q)
-    rhs = torch.empty_like(q) if a.op in ("volume", "surface", "rhs", "update") else None
+    rhs = q2   # (volume / surface / rhs write it; no fourth state buffer: the fill boxes hold three)
     for _ in range(a.reps):
         if a.op == "stage":
             sy.stage_into(q, q2, res, RK4A[1], RK4B[1], 1e-3, a.lift)
@@ -54,7 +54,7 @@ def main():
         elif a.op == "rhs":
             sy.rhs_into(q, rhs, a.lift)
         else:
-            _device_update(q2, res, rhs, RK4A[1], RK4B[1], 1e-3)
+            _device_update(q2, res, q, RK4A[1], RK4B[1], 1e-3)   # as bench.py's breakdown
     torch.cuda.synchronize()
 
 

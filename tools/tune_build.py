@@ -24,7 +24,9 @@ VARIANTS = {
     "ept4": ["-DBBDG_EPT_MAX_N=4"],                            # fp32 N=4 on the register kernel
     "nonb": ["-DBBDG_EXP_NO_NB=1"],
     "nonb64": ["-DBBDG_EXP_NO_NB=1"],
-    "eptold": ["-DBBDG_EPT_LOCNB=0"],                          # EPT without the in-tile neighbour copies
+    "eptold": ["-DBBDG_EPT_LOCNB=0"],
+    "shf2": ["-DBBDG_OPT_SHF4=0,1,1,1,2,2,2,2,2,2"],          # cascade levels read by shuffles up to 2 parent slots
+    "shf0": ["-DBBDG_OPT_SHF4=0,0,0,0,0,0,0,0,0,0"],          # no shuffle levels                          # EPT without the in-tile neighbour copies
     "loc64": ["-DBBDG_OPT_LOCNB8=0,0,0,1,1,1,1,1,1,1"],        # fp64: in-tile neighbour traces at N >= 3                              # experiment: no neighbour gather (wrong results)
 }
 

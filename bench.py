@@ -509,7 +509,7 @@ def main():
                        "d2h_bytes_per_step": e2e["bytes_per_step"], "pageable_value": e2e["pageable_value"],
                        "what": f"lsrk4_step (5 fused stages) on a host numpy state per order, {e2e['mesh']}: H2D + "
                                "stages + D2H in the timed region (pinned: chunk-pipelined bbdg_step_host; "
-                               "pageable_value: an ordinary numpy array)", "per_order": e2e["per_order"]}
+                               "pageable_value: an ordinary numpy array through the pinned staging rings of bbdg_step_pageable)", "per_order": e2e["per_order"]}
     else:
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                        "what": "not measured in --quick / --no-e2e / multi-GPU mode"}

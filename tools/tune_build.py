@@ -25,6 +25,8 @@ VARIANTS = {
     "nonb": ["-DBBDG_EXP_NO_NB=1"],
     "nonb64": ["-DBBDG_EXP_NO_NB=1"],
     "eptold": ["-DBBDG_EPT_LOCNB=0"],
+    "kc8": ["-DBBDG_TC_KC=8"],                                 # tcgen05 nodal: 8-wide K chunks (more stages)
+    "kc32": ["-DBBDG_TC_KC=32"],                               # tcgen05 nodal: 32-wide K chunks
     "shf2": ["-DBBDG_OPT_SHF4=0,1,1,1,2,2,2,2,2,2"],          # cascade levels read by shuffles up to 2 parent slots
     "shf0": ["-DBBDG_OPT_SHF4=0,0,0,0,0,0,0,0,0,0"],          # no shuffle levels                          # EPT without the in-tile neighbour copies
     "loc64": ["-DBBDG_OPT_LOCNB8=0,0,0,1,1,1,1,1,1,1"],        # fp64: in-tile neighbour traces at N >= 3                              # experiment: no neighbour gather (wrong results)
